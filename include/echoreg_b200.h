@@ -1,0 +1,165 @@
+/*
+ * echoreg_b200.h -- C ABI of the B200 (sm_100a) SMC rigid-registration path.
+ *
+ * Drop-in boundary for the reference's kernel-module seam
+ * (/root/reference/pkg/src/echoreg/backend.py:33-108 selects a module that
+ * exports NAME, ncc_measure_batch, resample_trilinear, warm_up --
+ * kernels_numba.py:22,192-233).  Plain pointers and sizes only: every
+ * pointer named *_dev is DEVICE memory owned by the caller, every `stream`
+ * is a cudaStream_t passed as void*.  All functions are asynchronous on
+ * `stream` unless stated and return 0 on success or an ER_E* code; the text
+ * of the last error is available from er_last_error().
+ *
+ * Volumes are C-order (nx, ny, nz) with k (z) fastest, the reference's
+ * in-memory layout (volume.py:33).  A volume may be stored as u8 / f32 /
+ * f64; the value the algorithm sees is  alpha * stored + gamma  (alpha = 1,
+ * gamma = 0 for a verbatim copy; raw uint8 echo data with the z-score of
+ * volume.py:119-130 folded in otherwise).
+ */
+#ifndef ECHOREG_B200_H
+#define ECHOREG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ER_OK 0
+#define ER_EINVAL 1     /* bad argument (maps to echoreg BadConfig / ValueError) */
+#define ER_ECUDA 2      /* CUDA runtime error (maps to echoreg InternalError) */
+#define ER_EWEIGHTS 3   /* weights failed to normalise (smc.py:139-142 check) */
+
+#define ER_U8 0
+#define ER_F32 1
+#define ER_F64 2
+
+/* Interpolation arithmetic of the measurement kernel. */
+#define ER_LERP_F32 0      /* fp32 lerps on fp64 coordinates/fractions      */
+#define ER_LERP_F64 1      /* fp64 lerps (FMA), fp64 everywhere             */
+#define ER_LERP_EXACT 2    /* fp64 lerps in the reference's a(1-f)+bf order */
+
+typedef struct er_volume {
+  const void *data_dev; /* device pointer */
+  int32_t dtype;        /* ER_U8 / ER_F32 / ER_F64 */
+  int32_t nx, ny, nz;
+  double alpha, gamma;  /* value = alpha * stored + gamma */
+} er_volume;
+
+int er_abi_version(void);
+const char *er_last_error(void);
+
+/* ---- volumes ---------------------------------------------------------- */
+
+/* Stored-value moments: out_dev[0] = sum(stored), out_dev[1] = sum(stored^2),
+ * deterministic fixed-order fp64 reduction.  Feeds the full-region target
+ * totals of kernels_numba.py:123-130.  out_dev must hold ER_MOMENTS_DOUBLES
+ * doubles (the tail is reduction scratch). */
+#define ER_MOMENTS_DOUBLES 1026
+int er_volume_moments(const er_volume *v, double *out_dev, void *stream);
+
+/* Classify an f64 device volume: flags_dev[0] = 1 if every voxel is 0 or 1
+ * (volume.py:138-140), flags_dev[1] = 1 if every voxel is exactly
+ * representable in fp32.  Used to pick a lossless storage type. */
+int er_classify_f64(const double *data_dev, int64_t n, int32_t *flags_dev, void *stream);
+
+/* Convert an f64 volume to u8 (values must be integers 0..255) or f32. */
+int er_convert_f64(const double *data_dev, int64_t n, int32_t dst_dtype, void *dst_dev,
+                   void *stream);
+
+/* ---- the hot path: fused pull-back trilinear resample + squared NCC ---- */
+/* Replaces kernels_numba.ncc_measure_batch / _ncc_kernel
+ * (kernels_numba.py:116-189, 203-223) and is what Executor.measure_ncc
+ * (backend.py:78-108) dispatches to.  A_dev: P x 9 (row-major 3x3 index
+ * affine, geometry.index_affine), b_dev: P x 3.  tgt_moments_dev: the
+ * er_volume_moments() of the target.  Outputs: squared NCC (f64), the
+ * degenerate flag, and the exact in-bounds voxel count per particle. */
+size_t er_measure_workspace_bytes(const er_volume *tgt, int64_t P);
+int er_measure_ncc(const er_volume *tgt, const er_volume *src, const double *tgt_moments_dev,
+                   const double *A_dev, const double *b_dev, int64_t P, int32_t overlap_only,
+                   int32_t lerp_mode, double *ncc_dev, uint8_t *degen_dev, int64_t *n_in_dev,
+                   void *workspace_dev, size_t workspace_bytes, void *stream);
+
+/* ---- SMC particle machinery (smc.py:145-259), all on device ------------ */
+
+/* init_particles (smc.py:145-157): states_dev[N x 6] ~ uniform(-lim, lim)
+ * from stream (seed, 0, 0, 0), bit-exact with numpy. */
+int er_smc_init(double *states_dev, int64_t n, uint64_t seed, const double lim[6],
+                void *stream);
+
+/* predict (smc.py:160-174): out = clip(in + sigma * N(0,1)_{(seed,1,k,i)},
+ * -clip, clip) for particles i in [0, n).  sigma/clip computed by the host
+ * exactly as the reference does. */
+int er_smc_predict(const double *states_in_dev, double *states_out_dev, int64_t n,
+                   uint64_t seed, int64_t k, const double sigma[6], const double clip[6],
+                   void *stream);
+
+/* to_matrix about `center` (geometry.py:87-99) + index_affine
+ * (geometry.py:136-152) for states [first, first + count). */
+int er_states_to_affine(const double *states_dev, int64_t first, int64_t count,
+                        const double center[3], const double tgt_spacing[3],
+                        const double tgt_origin[3], const double src_spacing[3],
+                        const double src_origin[3], double *A_dev, double *b_dev,
+                        void *stream);
+
+/* Exhaustive grid nodes [first, first + count) of a GridSpec
+ * (exhaustive.py:25-75, lexicographic, last axis fastest) straight to
+ * index affines.  axis_step[6] in internal units (radians, mm). */
+int er_grid_to_affine(int64_t first, int64_t count, const int32_t half_counts[6],
+                      const double axis_step[6], const double center[3],
+                      const double tgt_spacing[3], const double tgt_origin[3],
+                      const double src_spacing[3], const double src_origin[3],
+                      double *states_dev, double *A_dev, double *b_dev, void *stream);
+
+/* First-max argmax over z_dev[0..n) folded into a running best with a strict
+ * '>' (exhaustive.py:106-109): best_dev = {value f64, index i64 (as f64 bits)}. */
+int er_argmax_update(const double *z_dev, int64_t n, int64_t base_index, double *best_dev,
+                     void *stream);
+
+/* One SMC update after measurement: best tracking (smc.py:203-206),
+ * update_weights (210-224), ess (227-229), resample_systematic with stream
+ * (seed, 2, k, 0) when ess < ess_fraction * n (232-248, 353-357), estimate
+ * (251-259) and the trace row (358-364).  Single CTA, no host round trip.
+ * ctl_dev layout: see er_smc_ctl below.  weights_dev is updated in place;
+ * states_out/z_out receive the (possibly resampled) population. */
+typedef struct er_smc_ctl {
+  double best_measurement; /* running best (init -1.0) */
+  double best_state[6];
+  int32_t has_best;
+  int32_t error;           /* ER_EWEIGHTS when |sum w - 1| > 1e-9 */
+} er_smc_ctl;
+
+#define ER_TRACE_STRIDE 12 /* estimate[6], mean, max, best, ess, fired, n_degenerate */
+
+int er_smc_update(const double *z_dev, const uint8_t *degen_dev, double *weights_dev,
+                  const double *states_in_dev, double *states_out_dev, double *z_out_dev,
+                  double *scratch_dev /* n doubles: cumulative weights */, int64_t n, double beta, double ess_fraction, uint64_t seed, int64_t k,
+                  int32_t estimate_best, er_smc_ctl *ctl_dev, double *trace_row_dev,
+                  void *stream);
+
+/* ---- warp / scoring of frames (geometry.py:188-200, metrics.py) -------- */
+
+/* resample_trilinear (kernels_numba.py:65-85, 192-200): pull `src` through
+ * the index affine onto an (nx, ny, nz) grid, fill 0, fp64 in the
+ * reference's operation order.  out_dev is f64. */
+int er_resample(const er_volume *src, const double A[9], const double b[3], int32_t nx,
+                int32_t ny, int32_t nz, double *out_dev, void *stream);
+
+/* dice_under_transform (metrics.py:88-93) as exact integer counts:
+ * counts_dev[0] = |moved > 0.5|, [1] = |target == 1|, [2] = |both|. */
+int er_warp_dice_counts(const er_volume *src_mask, const double A[9], const double b[3],
+                        const er_volume *tgt_mask, int64_t *counts_dev, void *stream);
+
+/* Two-pass squared-NCC sums of (tgt, warp(src)) over the full grid
+ * (metrics.py:49-68): out_dev = {sst, sss, sts, n}; out_dev must hold
+ * ER_NCC_SUMS_DOUBLES doubles (the tail is reduction scratch).  With
+ * identity != 0 the source is read on the target grid unwarped. */
+#define ER_NCC_SUMS_DOUBLES 1782
+int er_warp_ncc_sums(const er_volume *tgt, const er_volume *src, const double A[9],
+                     const double b[3], int32_t identity, double *out_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ECHOREG_B200_H */

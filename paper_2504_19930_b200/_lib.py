@@ -1,0 +1,131 @@
+"""ctypes binding of the sm_100a C-ABI library (include/echoreg_b200.h).
+
+There is no fallback: if the library is missing or no CUDA device is
+present, every entry point raises ``InternalError`` (the reference's exit
+code 3 class) instead of silently computing on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import BadConfig, InternalError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libechoreg_sm100.so")
+
+ER_OK, ER_EINVAL, ER_ECUDA, ER_EWEIGHTS = 0, 1, 2, 3
+ER_U8, ER_F32, ER_F64 = 0, 1, 2
+ER_LERP_F32, ER_LERP_F64, ER_LERP_EXACT = 0, 1, 2
+ER_MOMENTS_DOUBLES = 1026
+ER_NCC_SUMS_DOUBLES = 1782
+ER_TRACE_STRIDE = 12
+
+_p = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_f64 = ctypes.c_double
+_d3 = ctypes.c_double * 3
+_d6 = ctypes.c_double * 6
+_d9 = ctypes.c_double * 9
+_i6 = ctypes.c_int32 * 6
+
+
+class ErVolume(ctypes.Structure):
+    _fields_ = [
+        ("data_dev", _p),
+        ("dtype", _i32),
+        ("nx", _i32),
+        ("ny", _i32),
+        ("nz", _i32),
+        ("alpha", _f64),
+        ("gamma", _f64),
+    ]
+
+
+class ErSmcCtl(ctypes.Structure):
+    _fields_ = [
+        ("best_measurement", _f64),
+        ("best_state", _f64 * 6),
+        ("has_best", _i32),
+        ("error", _i32),
+    ]
+
+
+_VP = ctypes.POINTER(ErVolume)
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "er_abi_version": (ctypes.c_int, []),
+    "er_last_error": (ctypes.c_char_p, []),
+    "er_volume_moments": (ctypes.c_int, [_VP, _p, _p]),
+    "er_classify_f64": (ctypes.c_int, [_p, _i64, _p, _p]),
+    "er_convert_f64": (ctypes.c_int, [_p, _i64, _i32, _p, _p]),
+    "er_measure_workspace_bytes": (ctypes.c_size_t, [_VP, _i64]),
+    "er_measure_ncc": (ctypes.c_int, [_VP, _VP, _p, _p, _p, _i64, _i32, _i32, _p, _p, _p,
+                                      _p, ctypes.c_size_t, _p]),
+    "er_smc_init": (ctypes.c_int, [_p, _i64, _u64, _d6, _p]),
+    "er_smc_predict": (ctypes.c_int, [_p, _p, _i64, _u64, _i64, _d6, _d6, _p]),
+    "er_states_to_affine": (ctypes.c_int, [_p, _i64, _i64, _d3, _d3, _d3, _d3, _d3, _p, _p,
+                                           _p]),
+    "er_grid_to_affine": (ctypes.c_int, [_i64, _i64, _i6, _d6, _d3, _d3, _d3, _d3, _d3, _p,
+                                         _p, _p, _p]),
+    "er_argmax_update": (ctypes.c_int, [_p, _i64, _i64, _p, _p]),
+    "er_smc_update": (ctypes.c_int, [_p, _p, _p, _p, _p, _p, _p, _i64, _f64, _f64, _u64,
+                                     _i64, _i32, _p, _p, _p]),
+    "er_resample": (ctypes.c_int, [_VP, _d9, _d3, _i32, _i32, _i32, _p, _p]),
+    "er_warp_dice_counts": (ctypes.c_int, [_VP, _d9, _d3, _VP, _p, _p]),
+    "er_warp_ncc_sums": (ctypes.c_int, [_VP, _VP, _d9, _d3, _i32, _p, _p]),
+}
+
+_lib = None
+
+
+def load():
+    """Load the shared library (no CUDA call is made here)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise InternalError(
+                f"sm_100a library not built: {LIB_PATH} missing "
+                "(run __graft_entry__.build()); there is no CPU fallback")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str = ""):
+    if rc == ER_OK:
+        return
+    msg = load().er_last_error().decode(errors="replace")
+    if rc == ER_EINVAL:
+        raise BadConfig(f"{what}: {msg}")
+    raise InternalError(f"{what}: {msg} (code {rc})")
+
+
+def call(name: str, *args):
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+    return rc
+
+
+def d3(v) -> "ctypes.Array":
+    return _d3(*[float(x) for x in v])
+
+
+def d6(v) -> "ctypes.Array":
+    return _d6(*[float(x) for x in v])
+
+
+def d9(v) -> "ctypes.Array":
+    return _d9(*[float(x) for x in v])
+
+
+def i6(v) -> "ctypes.Array":
+    return _i6(*[int(x) for x in v])

@@ -1,0 +1,88 @@
+"""The operator seam: Executor.measure_ncc (reference backend.py:56-108).
+
+``Executor`` keeps the reference's frozen-dataclass shape and its
+``measure_ncc(target, source, mats, overlap_only) -> (ncc, degenerate)``
+signature (tests subclass it, reference tests/test_exhaustive.py:114-117).
+It dispatches to the sm_100a kernels -- there is exactly one backend.
+``workers`` is accepted and validated for drop-in compatibility; device
+parallelism is ``torch.distributed`` ranks (one process per GPU), see
+``dist.py``.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import kernels_sm100, ops
+from .device import device_volume, require_cuda, torch
+from .errors import BadConfig
+from .geometry import index_affine_batch
+from .volume import Volume3
+
+BACKEND_ENV = "ECHOREG_BACKEND"
+_ACCEPTED = ("auto", "sm100")
+
+
+def get_backend(name: str | None = None):
+    """Resolve the kernel module (backend.py:33-53).  Only the sm_100a module
+    exists; asking for the reference's CPU backends is a configuration error."""
+    requested = (name or os.environ.get(BACKEND_ENV) or "auto").lower()
+    if requested not in _ACCEPTED:
+        raise BadConfig(
+            f"unknown backend {requested!r}; this build provides only 'sm100' "
+            "(alias 'auto') -- there is no CPU fallback")
+    return kernels_sm100
+
+
+def active_backend_name(name: str | None = None) -> str:
+    return get_backend(name).NAME
+
+
+@dataclass(frozen=True)
+class Executor:
+    """Device policy for data-parallel evaluations.
+
+    Results are identical for any worker or GPU count: every particle's
+    reduction runs on one GPU in a fixed order.
+    """
+
+    workers: int = 1
+    backend: str | None = None
+    precision: str = "f64"   # interpolation arithmetic: f32 | f64 | exact
+    device: int | None = None
+
+    def __post_init__(self):
+        if self.workers < 1:
+            raise BadConfig(f"worker count must be >= 1, got {self.workers}")
+        get_backend(self.backend)
+        ops.lerp_code(self.precision)
+
+    @property
+    def module(self):
+        return get_backend(self.backend)
+
+    def measure_ncc(self, target: Volume3, source: Volume3, mats: np.ndarray,
+                    overlap_only: bool = False):
+        """Squared NCC of the target against the source pulled through each
+        4x4 transform in mats; returns (ncc, degenerate) host arrays."""
+        mats = np.asarray(mats, dtype=np.float64)
+        if mats.ndim == 2:
+            mats = mats[np.newaxis]
+        a, b = index_affine_batch(mats, source.spacing, source.origin, target.spacing,
+                                  target.origin)
+        z, dg = self.measure_affine(target, source, a, b, overlap_only)
+        return z.cpu().numpy(), dg.cpu().numpy().astype(bool)
+
+    def measure_affine(self, target, source, a, b, overlap_only=False):
+        """Device-tensor variant on precomputed index affines (P,3,3)/(P,3)."""
+        dev = require_cuda(self.device)
+        t = torch()
+        tdv = device_volume(target, dev)
+        sdv = device_volume(source, dev)
+        A = t.as_tensor(np.ascontiguousarray(a, dtype=np.float64).reshape(-1, 9), device=dev)
+        B = t.as_tensor(np.ascontiguousarray(b, dtype=np.float64).reshape(-1, 3), device=dev)
+        z, dg, _ = ops.measure(tdv, sdv, A, B, overlap_only, self.precision)
+        return z, dg

@@ -1,0 +1,420 @@
+// The hot path: fused pull-back trilinear resample + squared NCC, one
+// likelihood per particle.  Replaces the reference's _ncc_kernel
+// (/root/reference/pkg/src/echoreg/kernels_numba.py:116-189).
+//
+// Decomposition (B200-first):
+//   * one CTA (256 threads, 8 warps) per (particle, tile of target planes);
+//     the tile shape depends only on the target dims, never on P or on the
+//     GPU count, so every particle's reduction order is fixed -> results are
+//     bitwise identical for any sharding (the reference's worker-invariance
+//     contract, kernels_numba.py:6-8).
+//   * a warp takes 32 target rows (i, j) at a time; lane r computes row r's
+//     in-bounds k-run with the reference's exact fp64 _k_interval
+//     (kernels_numba.py:88-113, 156-158) -> the in-bounds voxel set and the
+//     overlap count n are bit-exact.  The warp then walks the non-empty rows,
+//     lanes strided over k (k is the contiguous axis, volume.py:33), so target
+//     reads are coalesced and the 8 source gathers of neighbouring lanes fall
+//     in the same or adjacent cache lines.
+//   * source coordinates u = u0 + a02*k are formed in fp64 exactly as the
+//     reference does (no FMA), fractions in fp64; the 7 lerps run in fp32,
+//     fp64, or fp64 in the reference's a(1-f)+bf order (lerp_mode).
+//   * per-thread fp64 accumulation of {sum x, sum x^2, sum y*x, sum y,
+//     sum y^2} over in-bounds voxels (x = interpolated stored source value,
+//     y = stored target value), fixed-order warp-shuffle + smem block
+//     reduction, one 48-byte partial per CTA, fixed-order finalize per
+//     particle.  No float atomics anywhere.
+//   * the value affine (value = alpha*stored + gamma, e.g. raw uint8 echo
+//     data with the z-score folded in) is applied once per particle in the
+//     finalize, so the gather moves 1 byte per corner for uint8 volumes.
+#include "common.cuh"
+
+namespace {
+
+struct Partial {
+  double x, xx, yx, y, yy;
+  long long n;
+};
+
+struct Geom {
+  int nx, ny, nz;
+  int sx, sy, sz;
+  int planes_per_tile, ntiles;
+  double limx, limy, limz;
+};
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kRowsPerTile = 2048;
+
+// kernels_numba.py:88-113, bit-exact (IEEE division, ceil/floor, same guards)
+__device__ __forceinline__ void k_interval(double c0, double slope, double limit, int& klo,
+                                           int& khi) {
+  if (slope == 0.0) {
+    if (!(0.0 <= c0 && c0 <= limit)) {
+      klo = 0;
+      khi = 0;
+    }
+    return;
+  }
+  double lo, hi;
+  if (slope > 0.0) {
+    lo = rn_div(rn_sub(0.0, c0), slope);
+    hi = rn_div(rn_sub(limit, c0), slope);
+  } else {
+    lo = rn_div(rn_sub(limit, c0), slope);
+    hi = rn_div(rn_sub(0.0, c0), slope);
+  }
+  if (lo > (double)klo) {
+    if (lo > (double)khi) {
+      klo = 0;
+      khi = 0;
+      return;
+    }
+    klo = (int)ceil(lo);
+  }
+  if (hi < (double)(khi - 1)) {
+    if (hi < (double)klo) {
+      klo = 0;
+      khi = 0;
+      return;
+    }
+    khi = (int)floor(hi) + 1;
+  }
+}
+
+// clamped cell + fraction (kernels_numba.py:32-55)
+__device__ __forceinline__ void cell(double u, int n, int& c0, int& c1, double& f) {
+  int a = __double2int_rd(u);
+  a = a < 0 ? 0 : a;
+  int b = a + 1;
+  if (b > n - 1) {
+    b = n - 1;
+    a = b > 0 ? b - 1 : 0;
+  }
+  c0 = a;
+  c1 = b;
+  f = rn_sub(u, (double)a);
+}
+
+template <typename T>
+__device__ __forceinline__ float ldf(const T* __restrict__ p, int i) {
+  return (float)__ldg(p + i);
+}
+template <typename T>
+__device__ __forceinline__ double ldd(const T* __restrict__ p, int i) {
+  return (double)__ldg(p + i);
+}
+
+// Trilinear sample of the stored source values at in-bounds (u, v, w).
+template <typename ST, int LERP>
+__device__ __forceinline__ double sample(const ST* __restrict__ src, double u, double v,
+                                         double w, const Geom& g) {
+  int i0, i1, j0, j1, k0, k1;
+  double fu, fv, fw;
+  cell(u, g.sx, i0, i1, fu);
+  cell(v, g.sy, j0, j1, fv);
+  cell(w, g.sz, k0, k1, fw);
+  const int o00 = (i0 * g.sy + j0) * g.sz;
+  const int o01 = (i0 * g.sy + j1) * g.sz;
+  const int o10 = (i1 * g.sy + j0) * g.sz;
+  const int o11 = (i1 * g.sy + j1) * g.sz;
+  if (LERP == ER_LERP_F32) {
+    const float x000 = ldf(src, o00 + k0), x100 = ldf(src, o10 + k0);
+    const float x010 = ldf(src, o01 + k0), x110 = ldf(src, o11 + k0);
+    const float x001 = ldf(src, o00 + k1), x101 = ldf(src, o10 + k1);
+    const float x011 = ldf(src, o01 + k1), x111 = ldf(src, o11 + k1);
+    const float a = (float)fu, b = (float)fv, c = (float)fw;
+    const float c00 = fmaf(a, x100 - x000, x000);
+    const float c10 = fmaf(a, x110 - x010, x010);
+    const float c01 = fmaf(a, x101 - x001, x001);
+    const float c11 = fmaf(a, x111 - x011, x011);
+    const float c0 = fmaf(b, c10 - c00, c00);
+    const float c1 = fmaf(b, c11 - c01, c01);
+    return (double)fmaf(c, c1 - c0, c0);
+  } else {
+    const double x000 = ldd(src, o00 + k0), x100 = ldd(src, o10 + k0);
+    const double x010 = ldd(src, o01 + k0), x110 = ldd(src, o11 + k0);
+    const double x001 = ldd(src, o00 + k1), x101 = ldd(src, o10 + k1);
+    const double x011 = ldd(src, o01 + k1), x111 = ldd(src, o11 + k1);
+    if (LERP == ER_LERP_F64) {
+      const double c00 = fma(fu, x100 - x000, x000);
+      const double c10 = fma(fu, x110 - x010, x010);
+      const double c01 = fma(fu, x101 - x001, x001);
+      const double c11 = fma(fu, x111 - x011, x011);
+      const double c0 = fma(fv, c10 - c00, c00);
+      const double c1 = fma(fv, c11 - c01, c01);
+      return fma(fw, c1 - c0, c0);
+    } else {  // reference order x*(1-f) + y*f, no contraction
+      const double gu = rn_sub(1.0, fu), gv = rn_sub(1.0, fv), gw = rn_sub(1.0, fw);
+      const double c00 = rn_add(rn_mul(x000, gu), rn_mul(x100, fu));
+      const double c10 = rn_add(rn_mul(x010, gu), rn_mul(x110, fu));
+      const double c01 = rn_add(rn_mul(x001, gu), rn_mul(x101, fu));
+      const double c11 = rn_add(rn_mul(x011, gu), rn_mul(x111, fu));
+      const double c0 = rn_add(rn_mul(c00, gv), rn_mul(c10, fv));
+      const double c1 = rn_add(rn_mul(c01, gv), rn_mul(c11, fv));
+      return rn_add(rn_mul(c0, gw), rn_mul(c1, fw));
+    }
+  }
+}
+
+template <typename TT, typename ST, int LERP>
+__global__ void __launch_bounds__(kThreads, 3)
+    measure_partials_kernel(const TT* __restrict__ tgt, const ST* __restrict__ src,
+                            const double* __restrict__ A, const double* __restrict__ B,
+                            const Geom g, Partial* __restrict__ part) {
+  const int tile = blockIdx.x % g.ntiles;
+  const long long p = blockIdx.x / g.ntiles;
+  const double* Ap = A + 9 * p;
+  const double* Bp = B + 3 * p;
+  const double a00 = Ap[0], a01 = Ap[1], a02 = Ap[2];
+  const double a10 = Ap[3], a11 = Ap[4], a12 = Ap[5];
+  const double a20 = Ap[6], a21 = Ap[7], a22 = Ap[8];
+  const double b0 = Bp[0], b1 = Bp[1], b2 = Bp[2];
+
+  const int i_begin = tile * g.planes_per_tile;
+  const int i_end = min(g.nx, i_begin + g.planes_per_tile);
+  const int R = (i_end - i_begin) * g.ny;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  double sx = 0.0, sxx = 0.0, syx = 0.0, sy = 0.0, syy = 0.0;
+  int cnt = 0;
+
+  for (int base = warp * 32; base < R; base += kThreads) {
+    const int r = base + lane;
+    int klo = 0, khi = 0, off = 0;
+    double u0 = 0.0, v0 = 0.0, w0 = 0.0;
+    if (r < R) {
+      const int i = i_begin + r / g.ny;
+      const int j = r - (r / g.ny) * g.ny;
+      const double di = (double)i, dj = (double)j;
+      // kernels_numba.py:152-154, left-to-right, no FMA
+      u0 = rn_add(rn_add(rn_mul(a00, di), rn_mul(a01, dj)), b0);
+      v0 = rn_add(rn_add(rn_mul(a10, di), rn_mul(a11, dj)), b1);
+      w0 = rn_add(rn_add(rn_mul(a20, di), rn_mul(a21, dj)), b2);
+      khi = g.nz;
+      k_interval(u0, a02, g.limx, klo, khi);
+      k_interval(v0, a12, g.limy, klo, khi);
+      k_interval(w0, a22, g.limz, klo, khi);
+      if (khi < klo) khi = klo;
+      off = (i * g.ny + j) * g.nz;
+    }
+    cnt += khi - klo;
+    unsigned rows = __ballot_sync(0xffffffffu, khi > klo);
+    while (rows) {
+      const int q = __ffs(rows) - 1;
+      rows &= rows - 1;
+      const int qlo = __shfl_sync(0xffffffffu, klo, q);
+      const int qhi = __shfl_sync(0xffffffffu, khi, q);
+      const int qoff = __shfl_sync(0xffffffffu, off, q);
+      const double qu = __shfl_sync(0xffffffffu, u0, q);
+      const double qv = __shfl_sync(0xffffffffu, v0, q);
+      const double qw = __shfl_sync(0xffffffffu, w0, q);
+#pragma unroll 2
+      for (int k = qlo + lane; k < qhi; k += 32) {
+        const double kd = (double)k;
+        // kernels_numba.py:160-162
+        const double u = rn_add(qu, rn_mul(a02, kd));
+        const double v = rn_add(qv, rn_mul(a12, kd));
+        const double w = rn_add(qw, rn_mul(a22, kd));
+        const double x = sample<ST, LERP>(src, u, v, w, g);
+        const double y = ldd(tgt, qoff + k);
+        sx += x;
+        sxx = fma(x, x, sxx);
+        syx = fma(y, x, syx);
+        sy += y;
+        syy = fma(y, y, syy);
+      }
+    }
+  }
+
+  // fixed-order block reduction
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_down_sync(0xffffffffu, sx, o);
+    sxx += __shfl_down_sync(0xffffffffu, sxx, o);
+    syx += __shfl_down_sync(0xffffffffu, syx, o);
+    sy += __shfl_down_sync(0xffffffffu, sy, o);
+    syy += __shfl_down_sync(0xffffffffu, syy, o);
+    cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  }
+  __shared__ double red[kWarps][5];
+  __shared__ long long redn[kWarps];
+  if (lane == 0) {
+    red[warp][0] = sx;
+    red[warp][1] = sxx;
+    red[warp][2] = syx;
+    red[warp][3] = sy;
+    red[warp][4] = syy;
+    redn[warp] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Partial out{0.0, 0.0, 0.0, 0.0, 0.0, 0};
+    for (int w = 0; w < kWarps; ++w) {
+      out.x += red[w][0];
+      out.xx += red[w][1];
+      out.yx += red[w][2];
+      out.y += red[w][3];
+      out.yy += red[w][4];
+      out.n += redn[w];
+    }
+    part[blockIdx.x] = out;
+  }
+}
+
+struct Affines {
+  double as, gs, at, gt;
+};
+
+// Per-particle finalize: kernels_numba.py:172-189 on the affine-corrected sums.
+__global__ void measure_finalize_kernel(const Partial* __restrict__ part, int ntiles,
+                                        long long P, const double* __restrict__ tmom,
+                                        double nvox, int overlap, Affines f,
+                                        double* __restrict__ ncc, uint8_t* __restrict__ degen,
+                                        int64_t* __restrict__ n_in) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  double X = 0.0, XX = 0.0, YX = 0.0, Y = 0.0, YY = 0.0;
+  long long n = 0;
+  const Partial* q = part + p * ntiles;
+  for (int t = 0; t < ntiles; ++t) {
+    X += q[t].x;
+    XX += q[t].xx;
+    YX += q[t].yx;
+    Y += q[t].y;
+    YY += q[t].yy;
+    n += q[t].n;
+  }
+  if (n_in) n_in[p] = n;
+  const double ni = (double)n;
+  // value-space sums over in-bounds voxels (out-of-bounds source = fill 0)
+  const double s_s = f.as * X + f.gs * ni;
+  const double s_ss = f.as * f.as * XX + 2.0 * f.as * f.gs * X + f.gs * f.gs * ni;
+  const double s_ts = f.at * f.as * YX + f.at * f.gs * Y + f.gt * f.as * X + f.gt * f.gs * ni;
+  double s_t, s_tt, nf;
+  if (overlap) {
+    s_t = f.at * Y + f.gt * ni;
+    s_tt = f.at * f.at * YY + 2.0 * f.at * f.gt * Y + f.gt * f.gt * ni;
+    nf = ni;
+  } else {
+    s_t = f.at * tmom[0] + f.gt * nvox;
+    s_tt = f.at * f.at * tmom[1] + 2.0 * f.at * f.gt * tmom[0] + f.gt * f.gt * nvox;
+    nf = nvox;
+  }
+  if (nf == 0.0) {
+    ncc[p] = 0.0;
+    degen[p] = 1;
+    return;
+  }
+  const double sst = rn_sub(s_tt, rn_div(rn_mul(s_t, s_t), nf));
+  const double sss = rn_sub(s_ss, rn_div(rn_mul(s_s, s_s), nf));
+  if (rn_div(sst, nf) < 1e-12 || rn_div(sss, nf) < 1e-12) {
+    ncc[p] = 0.0;
+    degen[p] = 1;
+  } else {
+    const double sts = rn_sub(s_ts, rn_div(rn_mul(s_t, s_s), nf));
+    ncc[p] = rn_div(rn_mul(sts, sts), rn_mul(sst, sss));
+    degen[p] = 0;
+  }
+}
+
+Geom make_geom(const er_volume* t, const er_volume* s) {
+  Geom g;
+  g.nx = t->nx;
+  g.ny = t->ny;
+  g.nz = t->nz;
+  g.sx = s->nx;
+  g.sy = s->ny;
+  g.sz = s->nz;
+  int ppt = kRowsPerTile / (g.ny > 0 ? g.ny : 1);
+  if (ppt < 1) ppt = 1;
+  if (ppt > g.nx) ppt = g.nx;
+  g.planes_per_tile = ppt;
+  g.ntiles = (g.nx + ppt - 1) / ppt;
+  g.limx = (double)g.sx - 1.0;
+  g.limy = (double)g.sy - 1.0;
+  g.limz = (double)g.sz - 1.0;
+  return g;
+}
+
+template <typename TT, typename ST, int LERP>
+void launch_typed(const er_volume* t, const er_volume* s, const double* A, const double* B,
+                  const Geom& g, Partial* part, long long P, cudaStream_t st) {
+  const long long blocks = P * g.ntiles;
+  measure_partials_kernel<TT, ST, LERP><<<(unsigned)blocks, kThreads, 0, st>>>(
+      (const TT*)t->data_dev, (const ST*)s->data_dev, A, B, g, part);
+}
+
+template <typename TT, typename ST>
+void launch_lerp(int lerp, const er_volume* t, const er_volume* s, const double* A,
+                 const double* B, const Geom& g, Partial* part, long long P, cudaStream_t st) {
+  switch (lerp) {
+    case ER_LERP_F32: launch_typed<TT, ST, ER_LERP_F32>(t, s, A, B, g, part, P, st); break;
+    case ER_LERP_F64: launch_typed<TT, ST, ER_LERP_F64>(t, s, A, B, g, part, P, st); break;
+    default: launch_typed<TT, ST, ER_LERP_EXACT>(t, s, A, B, g, part, P, st); break;
+  }
+}
+
+template <typename TT>
+void launch_src(int lerp, const er_volume* t, const er_volume* s, const double* A,
+                const double* B, const Geom& g, Partial* part, long long P, cudaStream_t st) {
+  switch (s->dtype) {
+    case ER_U8: launch_lerp<TT, uint8_t>(lerp, t, s, A, B, g, part, P, st); break;
+    case ER_F32: launch_lerp<TT, float>(lerp, t, s, A, B, g, part, P, st); break;
+    default: launch_lerp<TT, double>(lerp, t, s, A, B, g, part, P, st); break;
+  }
+}
+
+bool valid_volume(const er_volume* v) {
+  if (!v || !v->data_dev) return false;
+  if (v->dtype < ER_U8 || v->dtype > ER_F64) return false;
+  if (v->nx < 1 || v->ny < 1 || v->nz < 1) return false;
+  const long long n = (long long)v->nx * v->ny * v->nz;
+  return n < (1LL << 31);
+}
+
+}  // namespace
+
+extern "C" size_t er_measure_workspace_bytes(const er_volume* tgt, int64_t P) {
+  if (!tgt || tgt->nx < 1 || tgt->ny < 1 || P < 0) return 0;
+  Geom g = make_geom(tgt, tgt);
+  return (size_t)P * (size_t)g.ntiles * sizeof(Partial);
+}
+
+extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
+                              const double* tgt_moments_dev, const double* A_dev,
+                              const double* b_dev, int64_t P, int32_t overlap_only,
+                              int32_t lerp_mode, double* ncc_dev, uint8_t* degen_dev,
+                              int64_t* n_in_dev, void* workspace_dev, size_t workspace_bytes,
+                              void* stream) {
+  if (!valid_volume(tgt) || !valid_volume(src))
+    return er_set_error(ER_EINVAL, "er_measure_ncc: invalid volume descriptor");
+  if (P < 0) return er_set_error(ER_EINVAL, "er_measure_ncc: negative particle count");
+  if (P == 0) return ER_OK;
+  if (!A_dev || !b_dev || !ncc_dev || !degen_dev || !tgt_moments_dev)
+    return er_set_error(ER_EINVAL, "er_measure_ncc: null pointer");
+  if (lerp_mode < ER_LERP_F32 || lerp_mode > ER_LERP_EXACT)
+    return er_set_error(ER_EINVAL, "er_measure_ncc: bad lerp_mode");
+  const Geom g = make_geom(tgt, src);
+  const size_t need = (size_t)P * (size_t)g.ntiles * sizeof(Partial);
+  if (!workspace_dev || workspace_bytes < need)
+    return er_set_error(ER_EINVAL, "er_measure_ncc: workspace too small");
+  if ((long long)P * g.ntiles >= (1LL << 31))
+    return er_set_error(ER_EINVAL, "er_measure_ncc: too many particles for one launch");
+  cudaStream_t st = as_stream(stream);
+  Partial* part = (Partial*)workspace_dev;
+  switch (tgt->dtype) {
+    case ER_U8: launch_src<uint8_t>(lerp_mode, tgt, src, A_dev, b_dev, g, part, P, st); break;
+    case ER_F32: launch_src<float>(lerp_mode, tgt, src, A_dev, b_dev, g, part, P, st); break;
+    default: launch_src<double>(lerp_mode, tgt, src, A_dev, b_dev, g, part, P, st); break;
+  }
+  ER_CHECK_LAUNCH();
+  Affines f{src->alpha, src->gamma, tgt->alpha, tgt->gamma};
+  const double nvox = (double)tgt->nx * (double)tgt->ny * (double)tgt->nz;
+  const int fb = 128;
+  measure_finalize_kernel<<<(unsigned)((P + fb - 1) / fb), fb, 0, st>>>(
+      part, g.ntiles, P, tgt_moments_dev, nvox, overlap_only ? 1 : 0, f, ncc_dev, degen_dev,
+      n_in_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}

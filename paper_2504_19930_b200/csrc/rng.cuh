@@ -1,0 +1,173 @@
+// Counter-based RNG that reproduces, bit for bit, the numpy streams the
+// reference draws from:
+//   _stream(seed, role, step, index) = Generator(Philox(key=seed,
+//       counter=[0, role, step, index]))            (echoreg/smc.py:38-42)
+// numpy's Philox4x64-10 pre-increments counter word 0 (with carry) before
+// every 4-word block, so block b of that stream is
+//   philox4x64_10(ctr = [b+1, role, step, index], key = [seed, 0]).
+// Doubles are (u64 >> 11) * 2^-53; Gaussians use numpy's 256-layer ziggurat
+// with numpy's own tables (gen_ziggurat.py).  The slow-path exp/log1p are
+// CUDA's; a 1-ulp difference from glibc could only flip an accept test that
+// lands within one ulp of its threshold (never observed, see tests/test_rng.py).
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#include "zig_tables.h"
+
+#if defined(__CUDACC__)
+#define ER_HD __host__ __device__ __forceinline__
+#else
+#define ER_HD inline
+#endif
+
+#if defined(__CUDACC__)
+// one translation unit (smc.cu) includes this header
+__constant__ uint64_t er_ki_double[256] = ER_KI_INIT;
+__constant__ double er_wi_double[256] = ER_WI_INIT;
+__constant__ double er_fi_double[256] = ER_FI_INIT;
+#endif
+static const uint64_t er_host_ki_double[256] = ER_KI_INIT;
+static const double er_host_wi_double[256] = ER_WI_INIT;
+static const double er_host_fi_double[256] = ER_FI_INIT;
+
+#ifdef __CUDA_ARCH__
+#define ER_KI er_ki_double
+#define ER_WI er_wi_double
+#define ER_FI er_fi_double
+#else
+#define ER_KI er_host_ki_double
+#define ER_WI er_host_wi_double
+#define ER_FI er_host_fi_double
+#endif
+
+struct ErPhilox {
+  uint64_t ctr[4];
+  uint64_t key[2];
+  uint64_t buf[4];
+  int pos;
+};
+
+ER_HD void er_mulhilo64(uint64_t a, uint64_t b, uint64_t* hi, uint64_t* lo) {
+#ifdef __CUDA_ARCH__
+  *lo = a * b;
+  *hi = __umul64hi(a, b);
+#else
+  unsigned __int128 p = (unsigned __int128)a * b;
+  *lo = (uint64_t)p;
+  *hi = (uint64_t)(p >> 64);
+#endif
+}
+
+// Philox4x64 with 10 rounds (Salmon et al., SC'11; the Random123 constants).
+ER_HD void er_philox4x64_10(const uint64_t in[4], const uint64_t key_in[2], uint64_t out[4]) {
+  const uint64_t M0 = 0xD2E7470EE14C6C93ULL, M1 = 0xCA5A826395121157ULL;
+  const uint64_t W0 = 0x9E3779B97F4A7C15ULL, W1 = 0xBB67AE8584CAA73BULL;
+  uint64_t c0 = in[0], c1 = in[1], c2 = in[2], c3 = in[3];
+  uint64_t k0 = key_in[0], k1 = key_in[1];
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += W0;
+      k1 += W1;
+    }
+    uint64_t hi0, lo0, hi1, lo1;
+    er_mulhilo64(M0, c0, &hi0, &lo0);
+    er_mulhilo64(M1, c2, &hi1, &lo1);
+    uint64_t n0 = hi1 ^ c1 ^ k0;
+    uint64_t n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+// Generator(Philox(key=seed, counter=[0, role, step, index])): fresh state,
+// empty buffer (numpy sets buffer_pos = 4).
+ER_HD void er_stream_init(ErPhilox* s, uint64_t seed, uint64_t role, uint64_t step, uint64_t index) {
+  s->ctr[0] = 0;
+  s->ctr[1] = role;
+  s->ctr[2] = step;
+  s->ctr[3] = index;
+  s->key[0] = seed;
+  s->key[1] = 0;
+  s->pos = 4;
+}
+
+// Jump straight to block b (0-based) of a fresh stream: used when element e
+// of a long draw sequence is wanted without generating 0..e-1.
+ER_HD void er_stream_seek_block(ErPhilox* s, uint64_t block) {
+  // the stream pre-increments: block b uses ctr[0] = b + 1 (carry into ctr[1..3])
+  uint64_t c0 = s->ctr[0] + block;
+  uint64_t carry = c0 < s->ctr[0];
+  s->ctr[0] = c0;
+  if (carry && ++s->ctr[1] == 0 && ++s->ctr[2] == 0) ++s->ctr[3];
+  s->pos = 4;
+}
+
+ER_HD uint64_t er_next_u64(ErPhilox* s) {
+  if (s->pos < 4) return s->buf[s->pos++];
+  if (++s->ctr[0] == 0 && ++s->ctr[1] == 0 && ++s->ctr[2] == 0) ++s->ctr[3];
+  er_philox4x64_10(s->ctr, s->key, s->buf);
+  s->pos = 1;
+  return s->buf[0];
+}
+
+ER_HD double er_u64_to_double(uint64_t r) {
+  return (double)(r >> 11) * (1.0 / 9007199254740992.0);
+}
+
+ER_HD double er_next_double(ErPhilox* s) { return er_u64_to_double(er_next_u64(s)); }
+
+#ifdef __CUDA_ARCH__
+#define ER_MUL(a, b) __dmul_rn((a), (b))
+#define ER_ADD(a, b) __dadd_rn((a), (b))
+#define ER_SUB(a, b) __dsub_rn((a), (b))
+#else
+#define ER_MUL(a, b) ((a) * (b))
+#define ER_ADD(a, b) ((a) + (b))
+#define ER_SUB(a, b) ((a) - (b))
+#endif
+
+// numpy random_standard_normal (ziggurat, 256 layers), numpy/random/src/
+// distributions/distributions.c; r = [idx:8 | sign:1 | rabs:52 | ...].
+ER_HD double er_standard_normal(ErPhilox* s) {
+  const double zr = 3.6541528853610087963519472518;      // ziggurat_nor_r
+  const double zinv = 0.27366123732975827203338247596;   // ziggurat_nor_inv_r
+  for (;;) {
+    uint64_t r = er_next_u64(s);
+    int idx = (int)(r & 0xff);
+    r >>= 8;
+    int sign = (int)(r & 0x1);
+    uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double x = ER_MUL((double)rabs, ER_WI[idx]);
+    if (sign) x = -x;
+    if (rabs < ER_KI[idx]) return x;
+    if (idx == 0) {
+      for (;;) {
+        double xx = ER_MUL(-zinv, log1p(-er_next_double(s)));
+        double yy = -log1p(-er_next_double(s));
+        if (ER_ADD(yy, yy) > ER_MUL(xx, xx))
+          return ((rabs >> 8) & 0x1) ? -ER_ADD(zr, xx) : ER_ADD(zr, xx);
+      }
+    } else {
+      double f = ER_ADD(ER_MUL(ER_SUB(ER_FI[idx - 1], ER_FI[idx]), er_next_double(s)), ER_FI[idx]);
+      if (f < exp(ER_MUL(ER_MUL(-0.5, x), x))) return x;
+    }
+  }
+}
+
+// element drawn from an already generated 64-bit word
+ER_HD double er_uniform_from(uint64_t r, double lower, double range) {
+  return ER_ADD(lower, ER_MUL(range, er_u64_to_double(r)));
+}
+
+// numpy random_uniform: lower + range * next_double (no FMA)
+ER_HD double er_uniform(ErPhilox* s, double lower, double range) {
+  return ER_ADD(lower, ER_MUL(range, er_next_double(s)));
+}

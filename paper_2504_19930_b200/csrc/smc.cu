@@ -1,0 +1,481 @@
+// SMC particle machinery on device (reference: echoreg/smc.py:145-259,
+// geometry.py:76-152, exhaustive.py:25-113).  Everything between two
+// measurements runs here, so an SMC iteration never round-trips to the host.
+#include "common.cuh"
+#include "rng.cuh"
+
+namespace {
+
+constexpr int kUpdThreads = 1024;
+
+// to_matrix (geometry.py:87-99) + index_affine (geometry.py:136-152),
+// naive left-to-right fp64 without contraction.  The reference's 3x3
+// products go through BLAS, which may round one ulp differently; ±1-ulp
+// matrix perturbations are parity-safe.
+struct AffineGeom {
+  double c[3];
+  double st[3], ot[3];  // target (reference grid) spacing / origin
+  double ss[3], os[3];  // source spacing / origin
+};
+
+__device__ void state_to_affine(const double* s, const AffineGeom& g, double* A, double* B) {
+  double sxr, cxr, syr, cyr, szr, czr;
+  sincos(s[0], &sxr, &cxr);
+  sincos(s[1], &syr, &cyr);
+  sincos(s[2], &szr, &czr);
+  // rotation_xyz: Rz @ Ry @ Rx (geometry.py:76-84)
+  const double m00 = rn_mul(czr, cyr), m01 = -szr, m02 = rn_mul(czr, syr);
+  const double m10 = rn_mul(szr, cyr), m11 = czr, m12 = rn_mul(szr, syr);
+  const double m20 = -syr, m21 = 0.0, m22 = cyr;
+  double R[3][3];
+  R[0][0] = m00;
+  R[0][1] = rn_add(rn_mul(m01, cxr), rn_mul(m02, sxr));
+  R[0][2] = rn_add(rn_mul(m01, -sxr), rn_mul(m02, cxr));
+  R[1][0] = m10;
+  R[1][1] = rn_add(rn_mul(m11, cxr), rn_mul(m12, sxr));
+  R[1][2] = rn_add(rn_mul(m11, -sxr), rn_mul(m12, cxr));
+  R[2][0] = m20;
+  R[2][1] = rn_add(rn_mul(m21, cxr), rn_mul(m22, sxr));
+  R[2][2] = rn_add(rn_mul(m21, -sxr), rn_mul(m22, cxr));
+  // t_m = R @ (t - c) + c
+  const double d0 = rn_sub(s[3], g.c[0]), d1 = rn_sub(s[4], g.c[1]), d2 = rn_sub(s[5], g.c[2]);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const double tm =
+        rn_add(rn_add(rn_add(rn_mul(R[r][0], d0), rn_mul(R[r][1], d1)), rn_mul(R[r][2], d2)), g.c[r]);
+    // index_affine: A = (R * st[None, :]) / ss[:, None];  b = (R @ ot + t - os) / ss
+#pragma unroll
+    for (int q = 0; q < 3; ++q) A[3 * r + q] = rn_div(rn_mul(R[r][q], g.st[q]), g.ss[r]);
+    const double rot =
+        rn_add(rn_add(rn_mul(R[r][0], g.ot[0]), rn_mul(R[r][1], g.ot[1])), rn_mul(R[r][2], g.ot[2]));
+    B[r] = rn_div(rn_sub(rn_add(rot, tm), g.os[r]), g.ss[r]);
+  }
+}
+
+__global__ void states_to_affine_kernel(const double* __restrict__ states, long long first,
+                                        long long count, AffineGeom g, double* __restrict__ A,
+                                        double* __restrict__ B) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  double s[6];
+#pragma unroll
+  for (int d = 0; d < 6; ++d) s[d] = states[6 * (first + q) + d];
+  state_to_affine(s, g, A + 9 * q, B + 3 * q);
+}
+
+struct GridAxes {
+  int half[6];
+  double step[6];
+};
+
+// exhaustive.py:51-75: node values arange(-m, m+1) * step, last axis fastest
+__global__ void grid_to_affine_kernel(long long first, long long count, GridAxes ax,
+                                      AffineGeom g, double* __restrict__ states,
+                                      double* __restrict__ A, double* __restrict__ B) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  long long rest = first + q;
+  double s[6];
+#pragma unroll
+  for (int a = 5; a >= 0; --a) {
+    const long long size = 2LL * ax.half[a] + 1;
+    const long long pos = rest % size;
+    rest /= size;
+    s[a] = rn_mul((double)(pos - ax.half[a]), ax.step[a]);
+  }
+  if (states) {
+#pragma unroll
+    for (int d = 0; d < 6; ++d) states[6 * q + d] = s[d];
+  }
+  state_to_affine(s, g, A + 9 * q, B + 3 * q);
+}
+
+// init_particles (smc.py:145-157): one stream for all N*6 values, C order.
+__global__ void smc_init_kernel(double* __restrict__ states, long long n, uint64_t seed,
+                                double lo0, double lo1, double lo2, double lo3, double lo4,
+                                double lo5, double rg0, double rg1, double rg2, double rg3,
+                                double rg4, double rg5) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const double lo[6] = {lo0, lo1, lo2, lo3, lo4, lo5};
+  const double rg[6] = {rg0, rg1, rg2, rg3, rg4, rg5};
+  const unsigned long long e0 = 6ULL * p;
+  uint64_t key[2] = {seed, 0};
+  uint64_t blk = ~0ULL, out[4];
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    const unsigned long long e = e0 + d;
+    const uint64_t b = e >> 2;
+    if (b != blk) {
+      uint64_t ctr[4] = {b + 1, 0, 0, 0};
+      er_philox4x64_10(ctr, key, out);
+      blk = b;
+    }
+    states[e] = er_uniform_from(out[e & 3], lo[d], rg[d]);
+  }
+}
+
+struct Six {
+  double v[6];
+};
+
+// predict (smc.py:160-174)
+__global__ void smc_predict_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                   long long n, uint64_t seed, long long k, Six sigma,
+                                   Six clip) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  ErPhilox s;
+  er_stream_init(&s, seed, 1, (uint64_t)k, (uint64_t)i);
+#pragma unroll 1
+  for (int d = 0; d < 6; ++d) {
+    const double z = er_standard_normal(&s);
+    double x = rn_add(in[6 * i + d], rn_mul(sigma.v[d], z));
+    x = fmax(x, -clip.v[d]);
+    x = fmin(x, clip.v[d]);
+    out[6 * i + d] = x;
+  }
+}
+
+// ---- single-CTA update: weights, ESS, systematic resampling, estimate ----
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fixed-order block sum; result broadcast to all threads
+__device__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double t = lane < (kUpdThreads / 32) ? sh[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) sh[32] = t;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
+// first-max argmax (np.argmax): larger value wins, ties -> lower index
+__device__ __forceinline__ void better(double& bv, long long& bi, double v, long long i) {
+  if (v > bv || (v == bv && i < bi)) {
+    bv = v;
+    bi = i;
+  }
+}
+
+__device__ void block_argmax(double& bv, long long& bi, double* shv, long long* shi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v = __shfl_down_sync(0xffffffffu, bv, o);
+    const long long i = __shfl_down_sync(0xffffffffu, bi, o);
+    better(bv, bi, v, i);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    shv[warp] = bv;
+    shi[warp] = bi;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    bv = lane < (kUpdThreads / 32) ? shv[lane] : -INFINITY;
+    bi = lane < (kUpdThreads / 32) ? shi[lane] : (1LL << 62);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v = __shfl_down_sync(0xffffffffu, bv, o);
+      const long long i = __shfl_down_sync(0xffffffffu, bi, o);
+      better(bv, bi, v, i);
+    }
+    if (lane == 0) {
+      shv[32] = bv;
+      shi[32] = bi;
+    }
+  }
+  __syncthreads();
+  bv = shv[32];
+  bi = shi[32];
+}
+
+// exclusive block scan of per-thread totals (fixed order)
+__device__ double block_exclusive_scan(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  __syncthreads();
+  if (lane == 31) sh[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    double w = lane < (kUpdThreads / 32) ? sh[lane] : 0.0;
+    double wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < (kUpdThreads / 32)) sh[lane] = wi - w;  // exclusive warp offsets
+  }
+  __syncthreads();
+  return sh[warp] + (incl - v);
+}
+
+__global__ void __launch_bounds__(kUpdThreads)
+    smc_update_kernel(const double* __restrict__ z, const uint8_t* __restrict__ degen,
+                      double* __restrict__ w, const double* __restrict__ st_in,
+                      double* __restrict__ st_out, double* __restrict__ z_out,
+                      double* __restrict__ cw, long long n, double beta, double ess_frac,
+                      uint64_t seed, long long k, int est_best, er_smc_ctl* __restrict__ ctl,
+                      double* __restrict__ trace) {
+  __shared__ double sh[40];
+  __shared__ double shv[40];
+  __shared__ long long shi[40];
+  __shared__ int fire_sh;
+  const int tid = threadIdx.x;
+  const long long chunk = (n + kUpdThreads - 1) / kUpdThreads;
+  const long long lo = min(n, tid * chunk), hi = min(n, lo + chunk);
+
+  // best tracking over this iteration's measurements (smc.py:203-206)
+  double bv = -INFINITY;
+  long long bi = 1LL << 62;
+  double ndeg = 0.0;
+  for (long long i = lo; i < hi; ++i) {
+    better(bv, bi, z[i], i);
+    ndeg += degen ? (double)degen[i] : 0.0;
+  }
+  block_argmax(bv, bi, shv, shi);
+  ndeg = block_sum(ndeg, sh);
+  if (tid == 0 && bv > ctl->best_measurement) {
+    ctl->best_measurement = bv;
+    ctl->has_best = 1;
+    for (int d = 0; d < 6; ++d) ctl->best_state[d] = st_in[6 * bi + d];
+  }
+
+  // update_weights (smc.py:210-224); beta >= 0 so max(beta*z) = beta*max(z)
+  const double m = rn_mul(beta, bv);
+  double part = 0.0;
+  for (long long i = lo; i < hi; ++i) {
+    const double wi = rn_mul(w[i], exp(rn_sub(rn_mul(beta, z[i]), m)));
+    w[i] = wi;
+    part += wi;
+  }
+  const double total = block_sum(part, sh);
+  const bool reset = !isfinite(total) || total <= 0.0;
+  double part2 = 0.0, psum = 0.0;
+  for (long long i = lo; i < hi; ++i) {
+    const double wi = reset ? rn_div(1.0, (double)n) : rn_div(w[i], total);
+    w[i] = wi;
+    part2 = fma(wi, wi, part2);
+    psum += wi;
+  }
+  const double wsum = block_sum(psum, sh);
+  const double w2 = block_sum(part2, sh);
+  const double ess = rn_div(1.0, w2);  // smc.py:227-229
+  if (tid == 0) {
+    if (fabs(wsum - 1.0) > 1e-9) ctl->error = ER_EWEIGHTS;  // smc.py:139-142
+    fire_sh = ess < rn_mul(ess_frac, (double)n);             // smc.py:353
+  }
+  __syncthreads();
+  const bool fire = fire_sh != 0;
+
+  if (fire) {
+    // resample_systematic (smc.py:232-248): u0 ~ U[0, 1/n) from (seed, 2, k, 0)
+    ErPhilox s;
+    er_stream_init(&s, seed, 2, (uint64_t)k, 0);
+    const double inv_n = rn_div(1.0, (double)n);
+    const double u0 = er_uniform(&s, 0.0, inv_n);
+    // cumsum: per-thread sequential chunk + block exclusive scan of chunk sums
+    double run = 0.0;
+    for (long long i = lo; i < hi; ++i) run += w[i];
+    double acc = block_exclusive_scan(run, sh);
+    for (long long i = lo; i < hi; ++i) {
+      acc += w[i];
+      cw[i] = acc;
+    }
+    __syncthreads();
+    __threadfence_block();
+    for (long long i = lo; i < hi; ++i) {
+      const double pos = rn_add(u0, rn_div((double)i, (double)n));
+      // searchsorted(cw, pos, side='right'): first index with cw > pos
+      long long a = 0, b = n;
+      while (a < b) {
+        const long long mid = (a + b) >> 1;
+        if (cw[mid] <= pos) a = mid + 1;
+        else b = mid;
+      }
+      const long long idx = a < n - 1 ? a : n - 1;
+#pragma unroll
+      for (int d = 0; d < 6; ++d) st_out[6 * i + d] = st_in[6 * idx + d];
+      z_out[i] = z[idx];
+    }
+    __syncthreads();
+    for (long long i = lo; i < hi; ++i) w[i] = inv_n;
+  } else {
+    for (long long i = lo; i < hi; ++i) {
+#pragma unroll
+      for (int d = 0; d < 6; ++d) st_out[6 * i + d] = st_in[6 * i + d];
+      z_out[i] = z[i];
+    }
+  }
+  __syncthreads();
+
+  // estimate (smc.py:251-259) and trace row (smc.py:358-364)
+  double est[6];
+  for (int d = 0; d < 6; ++d) {
+    double e = 0.0;
+    for (long long i = lo; i < hi; ++i) e = fma(w[i], st_out[6 * i + d], e);
+    est[d] = block_sum(e, sh);
+  }
+  double zs = 0.0, zmax = -INFINITY;
+  long long zi = 0;
+  for (long long i = lo; i < hi; ++i) {
+    zs += z_out[i];
+    better(zmax, zi, z_out[i], i);
+  }
+  const double zsum = block_sum(zs, sh);
+  block_argmax(zmax, zi, shv, shi);
+  if (tid == 0) {
+    const bool use_best = est_best && ctl->has_best;
+    for (int d = 0; d < 6; ++d) trace[d] = use_best ? ctl->best_state[d] : est[d];
+    trace[6] = rn_div(zsum, (double)n);
+    trace[7] = zmax;
+    trace[8] = ctl->best_measurement;
+    trace[9] = ess;
+    trace[10] = fire ? 1.0 : 0.0;
+    trace[11] = ndeg;
+  }
+}
+
+__global__ void argmax_update_kernel(const double* __restrict__ z, long long n,
+                                     long long base, double* __restrict__ best) {
+  __shared__ double shv[40];
+  __shared__ long long shi[40];
+  double bv = -INFINITY;
+  long long bi = 1LL << 62;
+  for (long long i = threadIdx.x; i < n; i += kUpdThreads) better(bv, bi, z[i], i);
+  block_argmax(bv, bi, shv, shi);
+  if (threadIdx.x == 0 && bv > best[0]) {  // strict '>' across chunks (exhaustive.py:107)
+    best[0] = bv;
+    best[1] = (double)(base + bi);
+  }
+}
+
+AffineGeom make_affine_geom(const double center[3], const double tsp[3], const double tor[3],
+                            const double ssp[3], const double sor[3]) {
+  AffineGeom g;
+  for (int d = 0; d < 3; ++d) {
+    g.c[d] = center[d];
+    g.st[d] = tsp[d];
+    g.ot[d] = tor[d];
+    g.ss[d] = ssp[d];
+    g.os[d] = sor[d];
+  }
+  return g;
+}
+
+}  // namespace
+
+extern "C" int er_smc_init(double* states_dev, int64_t n, uint64_t seed, const double lim[6],
+                           void* stream) {
+  if (!states_dev || !lim || n < 0) return er_set_error(ER_EINVAL, "er_smc_init: args");
+  if (n == 0) return ER_OK;
+  // numpy uniform(low=-lim, high=lim): range = high - low (computed in fp64)
+  double lo[6], rg[6];
+  for (int d = 0; d < 6; ++d) {
+    lo[d] = -lim[d];
+    rg[d] = lim[d] - (-lim[d]);
+  }
+  smc_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+      states_dev, n, seed, lo[0], lo[1], lo[2], lo[3], lo[4], lo[5], rg[0], rg[1], rg[2],
+      rg[3], rg[4], rg[5]);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_smc_predict(const double* states_in_dev, double* states_out_dev, int64_t n,
+                              uint64_t seed, int64_t k, const double sigma[6],
+                              const double clip[6], void* stream) {
+  if (!states_in_dev || !states_out_dev || !sigma || !clip || n < 0)
+    return er_set_error(ER_EINVAL, "er_smc_predict: args");
+  if (n == 0) return ER_OK;
+  Six sg, cl;
+  for (int d = 0; d < 6; ++d) {
+    sg.v[d] = sigma[d];
+    cl.v[d] = clip[d];
+  }
+  smc_predict_kernel<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(
+      states_in_dev, states_out_dev, n, seed, k, sg, cl);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_states_to_affine(const double* states_dev, int64_t first, int64_t count,
+                                   const double center[3], const double tgt_spacing[3],
+                                   const double tgt_origin[3], const double src_spacing[3],
+                                   const double src_origin[3], double* A_dev, double* b_dev,
+                                   void* stream) {
+  if (!states_dev || !A_dev || !b_dev || count < 0 || first < 0)
+    return er_set_error(ER_EINVAL, "er_states_to_affine: args");
+  if (count == 0) return ER_OK;
+  AffineGeom g = make_affine_geom(center, tgt_spacing, tgt_origin, src_spacing, src_origin);
+  states_to_affine_kernel<<<(unsigned)((count + 127) / 128), 128, 0, as_stream(stream)>>>(
+      states_dev, first, count, g, A_dev, b_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_grid_to_affine(int64_t first, int64_t count, const int32_t half_counts[6],
+                                 const double axis_step[6], const double center[3],
+                                 const double tgt_spacing[3], const double tgt_origin[3],
+                                 const double src_spacing[3], const double src_origin[3],
+                                 double* states_dev, double* A_dev, double* b_dev,
+                                 void* stream) {
+  if (!A_dev || !b_dev || count < 0 || first < 0 || !half_counts || !axis_step)
+    return er_set_error(ER_EINVAL, "er_grid_to_affine: args");
+  if (count == 0) return ER_OK;
+  GridAxes ax;
+  for (int a = 0; a < 6; ++a) {
+    if (half_counts[a] < 0) return er_set_error(ER_EINVAL, "er_grid_to_affine: half count");
+    ax.half[a] = half_counts[a];
+    ax.step[a] = axis_step[a];
+  }
+  AffineGeom g = make_affine_geom(center, tgt_spacing, tgt_origin, src_spacing, src_origin);
+  grid_to_affine_kernel<<<(unsigned)((count + 127) / 128), 128, 0, as_stream(stream)>>>(
+      first, count, ax, g, states_dev, A_dev, b_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_argmax_update(const double* z_dev, int64_t n, int64_t base_index,
+                                double* best_dev, void* stream) {
+  if (!z_dev || !best_dev || n < 0) return er_set_error(ER_EINVAL, "er_argmax_update: args");
+  if (n == 0) return ER_OK;
+  argmax_update_kernel<<<1, kUpdThreads, 0, as_stream(stream)>>>(z_dev, n, base_index, best_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_smc_update(const double* z_dev, const uint8_t* degen_dev, double* weights_dev,
+                             const double* states_in_dev, double* states_out_dev,
+                             double* z_out_dev, double* scratch_dev, int64_t n, double beta,
+                             double ess_fraction, uint64_t seed, int64_t k,
+                             int32_t estimate_best, er_smc_ctl* ctl_dev, double* trace_row_dev,
+                             void* stream) {
+  if (!z_dev || !weights_dev || !states_in_dev || !states_out_dev || !z_out_dev ||
+      !scratch_dev || !ctl_dev || !trace_row_dev || n < 1)
+    return er_set_error(ER_EINVAL, "er_smc_update: args");
+  if (beta < 0) return er_set_error(ER_EINVAL, "er_smc_update: beta must be >= 0");
+  smc_update_kernel<<<1, kUpdThreads, 0, as_stream(stream)>>>(
+      z_dev, degen_dev, weights_dev, states_in_dev, states_out_dev, z_out_dev, scratch_dev, n,
+      beta, ess_fraction, seed, k, estimate_best, ctl_dev, trace_row_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}

@@ -1,0 +1,147 @@
+// Volume-level device utilities: deterministic moments (the reference's
+// full-region target totals, kernels_numba.py:123-130), lossless storage
+// classification and conversion of fp64 volumes (volume.py:33 holds fp64).
+#include "common.cuh"
+
+namespace {
+
+constexpr int kMomBlocks = 512;  // fixed partition -> device-independent order
+constexpr int kMomThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kMomThreads)
+    moments_partial_kernel(const T* __restrict__ v, long long n, double* __restrict__ part) {
+  const long long lo = n * blockIdx.x / kMomBlocks;
+  const long long hi = n * (blockIdx.x + 1) / kMomBlocks;
+  double s = 0.0, ss = 0.0;
+  for (long long q = lo + threadIdx.x; q < hi; q += kMomThreads) {
+    const double x = (double)__ldg(v + q);
+    s += x;
+    ss = fma(x, x, ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    ss += __shfl_down_sync(0xffffffffu, ss, o);
+  }
+  __shared__ double red[kMomThreads / 32][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red[warp][0] = s;
+    red[warp][1] = ss;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < kMomThreads / 32; ++w) {
+      a += red[w][0];
+      b += red[w][1];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void moments_final_kernel(const double* __restrict__ part, double* __restrict__ out) {
+  // one warp, fixed order: lane-strided partial sums then shuffle tree
+  double s = 0.0, ss = 0.0;
+  for (int b = threadIdx.x; b < kMomBlocks; b += 32) {
+    s += part[2 * b];
+    ss += part[2 * b + 1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    ss += __shfl_down_sync(0xffffffffu, ss, o);
+  }
+  if (threadIdx.x == 0) {
+    out[0] = s;
+    out[1] = ss;
+  }
+}
+
+__global__ void classify_kernel(const double* __restrict__ v, long long n, int* __restrict__ flags) {
+  bool binary = true, f32 = true, u8 = true;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const double x = v[q];
+    binary &= (x == 0.0) | (x == 1.0);
+    f32 &= ((double)(float)x == x);
+    u8 &= (x >= 0.0) & (x <= 255.0) & (x == floor(x));
+  }
+  binary = __all_sync(0xffffffffu, binary);
+  f32 = __all_sync(0xffffffffu, f32);
+  u8 = __all_sync(0xffffffffu, u8);
+  if ((threadIdx.x & 31) == 0) {
+    if (!binary) atomicAnd(flags + 0, 0);
+    if (!f32) atomicAnd(flags + 1, 0);
+    if (!u8) atomicAnd(flags + 2, 0);
+  }
+}
+
+__global__ void init_flags_kernel(int* flags) {
+  if (threadIdx.x < 3) flags[threadIdx.x] = 1;
+}
+
+template <typename D>
+__global__ void convert_kernel(const double* __restrict__ v, long long n, D* __restrict__ out) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x)
+    out[q] = (D)v[q];
+}
+
+template <typename T>
+void launch_moments(const void* data, long long n, double* part, cudaStream_t st) {
+  moments_partial_kernel<T><<<kMomBlocks, kMomThreads, 0, st>>>((const T*)data, n, part);
+}
+
+}  // namespace
+
+extern "C" int er_volume_moments(const er_volume* v, double* out_dev, void* stream) {
+  if (!v || !v->data_dev || !out_dev) return er_set_error(ER_EINVAL, "er_volume_moments: null");
+  const long long n = (long long)v->nx * v->ny * v->nz;
+  if (n < 1) return er_set_error(ER_EINVAL, "er_volume_moments: empty volume");
+  cudaStream_t st = as_stream(stream);
+  // partials live right after the two outputs: caller allocates 2 + 2*512 doubles
+  double* part = out_dev + 2;
+  switch (v->dtype) {
+    case ER_U8: launch_moments<uint8_t>(v->data_dev, n, part, st); break;
+    case ER_F32: launch_moments<float>(v->data_dev, n, part, st); break;
+    case ER_F64: launch_moments<double>(v->data_dev, n, part, st); break;
+    default: return er_set_error(ER_EINVAL, "er_volume_moments: bad dtype");
+  }
+  ER_CHECK_LAUNCH();
+  moments_final_kernel<<<1, 32, 0, st>>>(part, out_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_classify_f64(const double* data_dev, int64_t n, int32_t* flags_dev,
+                               void* stream) {
+  if (!data_dev || !flags_dev || n < 0) return er_set_error(ER_EINVAL, "er_classify_f64: args");
+  cudaStream_t st = as_stream(stream);
+  init_flags_kernel<<<1, 32, 0, st>>>(flags_dev);
+  if (n > 0) {
+    long long blocks = (n + 255) / 256;
+    if (blocks > ER_NUM_SMS_B200 * 8) blocks = ER_NUM_SMS_B200 * 8;
+    classify_kernel<<<(unsigned)blocks, 256, 0, st>>>(data_dev, n, flags_dev);
+  }
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_convert_f64(const double* data_dev, int64_t n, int32_t dst_dtype,
+                              void* dst_dev, void* stream) {
+  if (!data_dev || !dst_dev || n < 0) return er_set_error(ER_EINVAL, "er_convert_f64: args");
+  if (n == 0) return ER_OK;
+  cudaStream_t st = as_stream(stream);
+  long long blocks = (n + 255) / 256;
+  if (blocks > ER_NUM_SMS_B200 * 8) blocks = ER_NUM_SMS_B200 * 8;
+  switch (dst_dtype) {
+    case ER_U8: convert_kernel<uint8_t><<<(unsigned)blocks, 256, 0, st>>>(data_dev, n, (uint8_t*)dst_dev); break;
+    case ER_F32: convert_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(data_dev, n, (float*)dst_dev); break;
+    default: return er_set_error(ER_EINVAL, "er_convert_f64: dst must be u8 or f32");
+  }
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}

@@ -1,0 +1,180 @@
+"""Device residency: volumes, streams and small buffers on the B200.
+
+PyTorch is used purely as the allocator/stream plumbing: tensors own the
+device memory, raw pointers go to the C ABI.  Every volume is uploaded once
+and cached on the (immutable) Volume3 object; its storage type is chosen
+losslessly:
+
+* codec hint (raw uint8 + z-score affine)   -> u8, alpha = 1/std, gamma = -mean/std
+* binary mask (volume.py:138-140)           -> u8, verbatim
+* integers in 0..255                        -> u8, verbatim
+* exactly fp32-representable                -> f32, verbatim
+* anything else                             -> f64, verbatim
+The classification runs on the device (er_classify_f64) on the fp64 upload.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import InternalError
+
+_torch = None
+_tls = threading.local()
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+
+        _torch = t
+    return _torch
+
+
+def require_cuda(device=None):
+    t = torch()
+    if not t.cuda.is_available():
+        raise InternalError(
+            "no CUDA device: the sm_100a path has no CPU fallback "
+            "(run on a B200 via gpurun)")
+    _lib.load()
+    return t.device("cuda", t.cuda.current_device() if device is None else int(device))
+
+
+def stream_ptr(device=None) -> ctypes.c_void_p:
+    t = torch()
+    s = t.cuda.current_stream(device)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ptr(tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(tensor.data_ptr())
+
+
+_DT = {_lib.ER_U8: "uint8", _lib.ER_F32: "float32", _lib.ER_F64: "float64"}
+
+
+@dataclass
+class DeviceVolume:
+    """A volume resident in HBM plus its C-ABI descriptor."""
+
+    storage: object          # torch tensor (flat)
+    desc: _lib.ErVolume
+    dims: tuple
+    spacing: tuple
+    origin: tuple
+    moments: object          # torch f64 [ER_MOMENTS_DOUBLES], [0]=sum, [1]=sumsq of stored
+    dtype_code: int
+
+    @property
+    def desc_ptr(self):
+        return ctypes.byref(self.desc)
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.storage.numel() * self.storage.element_size())
+
+
+def _make_desc(storage, code, dims, alpha, gamma):
+    d = _lib.ErVolume()
+    d.data_dev = storage.data_ptr()
+    d.dtype = code
+    d.nx, d.ny, d.nz = (int(x) for x in dims)
+    d.alpha = float(alpha)
+    d.gamma = float(gamma)
+    return d
+
+
+def upload_array(data: np.ndarray, device, *, codec=None, pinned_staging=False):
+    """Upload one fp64 (or raw uint8 codec) volume and pick its storage type."""
+    t = torch()
+    dims = tuple(int(x) for x in data.shape)
+    if len(dims) != 3:
+        raise ValueError("volume must be 3D")
+    if int(np.prod(dims)) >= 2**31:
+        raise ValueError("volume too large for one device descriptor (>= 2^31 voxels)")
+    stream = stream_ptr(device)
+    if codec is not None:
+        raw = np.ascontiguousarray(codec.raw, dtype=np.uint8).reshape(-1)
+        host = t.from_numpy(raw)
+        if pinned_staging:
+            host = host.pin_memory()
+        storage = host.to(device, non_blocking=pinned_staging)
+        code, alpha, gamma = _lib.ER_U8, 1.0 / codec.std, -codec.mean / codec.std
+    else:
+        flat = np.ascontiguousarray(data, dtype=np.float64).reshape(-1)
+        host = t.from_numpy(flat)
+        if pinned_staging:
+            host = host.pin_memory()
+        f64 = host.to(device, non_blocking=pinned_staging)
+        flags = t.empty(3, dtype=t.int32, device=device)
+        _lib.call("er_classify_f64", ptr(f64), f64.numel(), ptr(flags), stream)
+        binary, f32ok, u8ok = (bool(x) for x in flags.tolist())
+        alpha, gamma = 1.0, 0.0
+        if binary or u8ok:
+            storage = t.empty(f64.numel(), dtype=t.uint8, device=device)
+            _lib.call("er_convert_f64", ptr(f64), f64.numel(), _lib.ER_U8, ptr(storage), stream)
+            code = _lib.ER_U8
+        elif f32ok:
+            storage = t.empty(f64.numel(), dtype=t.float32, device=device)
+            _lib.call("er_convert_f64", ptr(f64), f64.numel(), _lib.ER_F32, ptr(storage), stream)
+            code = _lib.ER_F32
+        else:
+            storage, code = f64, _lib.ER_F64
+    desc = _make_desc(storage, code, dims, alpha, gamma)
+    moments = t.empty(_lib.ER_MOMENTS_DOUBLES, dtype=t.float64, device=device)
+    _lib.call("er_volume_moments", ctypes.byref(desc), ptr(moments), stream)
+    return storage, desc, moments, code
+
+
+def device_volume(v, device=None) -> DeviceVolume:
+    """Device copy of a Volume3 (cached on the object; volumes are immutable)."""
+    dev = require_cuda(device)
+    cache = getattr(v, "_er_device_cache", None)
+    if cache is None:
+        cache = {}
+        object.__setattr__(v, "_er_device_cache", cache)
+    key = dev.index
+    hit = cache.get(key)
+    if hit is not None:
+        return hit
+    storage, desc, moments, code = upload_array(v.data, dev, codec=getattr(v, "codec", None))
+    dv = DeviceVolume(storage, desc, tuple(v.dims), tuple(v.spacing), tuple(v.origin), moments,
+                      code)
+    cache[key] = dv
+    return dv
+
+
+def device_volume_from_array(data: np.ndarray, device=None, spacing=(1.0, 1.0, 1.0),
+                             origin=(0.0, 0.0, 0.0), pinned_staging=False) -> DeviceVolume:
+    """Uncached upload of a bare array (kernel-module seam: arrays, not Volume3)."""
+    dev = require_cuda(device)
+    storage, desc, moments, code = upload_array(np.asarray(data), dev,
+                                                pinned_staging=pinned_staging)
+    return DeviceVolume(storage, desc, tuple(int(x) for x in data.shape), tuple(spacing),
+                        tuple(origin), moments, code)
+
+
+class Workspace:
+    """Grow-only per-device scratch for the measurement partials."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, device, nbytes: int):
+        t = torch()
+        key = (device.index if hasattr(device, "index") else int(device))
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = t.empty(max(int(nbytes), 1), dtype=t.uint8, device=device)
+            self._bufs[key] = buf
+        return buf
+
+
+WORKSPACE = Workspace()

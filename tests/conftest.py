@@ -1,0 +1,51 @@
+"""Shared test setup.
+
+Markers: ``gpu`` tests need a B200 (run on the GPU box with ``-m gpu``);
+everything else runs on the CPU build box.  CPU tests exercise the oracle
+against the reference's golden vectors, the host logic, and that the C-ABI
+library loads and exports every declared symbol.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+def golden(name):
+    return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
+
+
+def golden_kernel_cases():
+    g = golden("kernels.npz")
+    names = [str(n) for n in g["case_names"]]
+    out = {}
+    for n in names:
+        prefix = f"{n}__"
+        out[n] = {k[len(prefix):]: g[k] for k in g.files if k.startswith(prefix)}
+    return out
+
+
+@pytest.fixture()
+def rng():
+    return np.random.default_rng(12345)
+
+
+def have_gpu():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False

@@ -1,0 +1,189 @@
+"""Parity of the sm_100a measurement kernel (the hot path) against the
+reference's own outputs (golden vectors) and the bit-exact C oracle.
+
+Tolerances (written here, per BASELINE north star): in-bounds voxel counts
+and degenerate flags bit-exact; per-particle squared NCC within 1e-4
+relative for the fp32-lerp mode, and within 1e-10 relative for the fp64
+modes (only the summation order differs from the reference there).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import kernels as ok
+
+from .conftest import golden, golden_kernel_cases
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+RTOL = {"f32": 1e-4, "f64": 1e-10, "exact": 1e-10}
+CASES = golden_kernel_cases()
+
+
+def _vol(data, spacing, origin):
+    from paper_2504_19930_b200 import Volume3
+
+    return Volume3(np.asarray(data), tuple(spacing), tuple(origin))
+
+
+def _measure(tgt, src, a, b, overlap, precision):
+    from paper_2504_19930_b200 import ops
+    from paper_2504_19930_b200.device import device_volume, require_cuda
+
+    dev = require_cuda()
+    A = torch.as_tensor(np.ascontiguousarray(a).reshape(-1, 9), device=dev)
+    B = torch.as_tensor(np.ascontiguousarray(b).reshape(-1, 3), device=dev)
+    z, d, n = ops.measure(device_volume(tgt, dev), device_volume(src, dev), A, B, overlap,
+                          precision)
+    return z.cpu().numpy(), d.cpu().numpy().astype(bool), n.cpu().numpy()
+
+
+def _close(got, want, rtol):
+    got, want = np.asarray(got), np.asarray(want)
+    scale = np.maximum(np.abs(want), 1e-300)
+    bad = np.abs(got - want) > rtol * scale + 1e-300
+    # exact zeros (degenerate) must stay exact zeros
+    bad |= (want == 0.0) != (got == 0.0)
+    return not bad.any(), float(np.max(np.abs(got - want) / scale))
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64", "exact"])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_measure_matches_reference_goldens(name, precision):
+    c = CASES[name]
+    tgt = _vol(c["tgt"], c["tgt_spacing"], c["tgt_origin"])
+    src = _vol(c["src"], c["src_spacing"], c["src_origin"])
+    for overlap, key in ((False, "full"), (True, "overlap")):
+        z, d, n = _measure(tgt, src, c["a"], c["b"], overlap, precision)
+        ok_, err = _close(z, c[f"ncc_{key}"], RTOL[precision])
+        assert ok_, (name, key, precision, err)
+        assert np.array_equal(d, c[f"degen_{key}"]), (name, key)
+        assert np.array_equal(n, c["n_in"]), (name, key)
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_executor_seam_matches_reference(precision):
+    from paper_2504_19930_b200 import Executor
+
+    c = CASES["cube10"]
+    tgt = _vol(c["tgt"], c["tgt_spacing"], c["tgt_origin"])
+    src = _vol(c["src"], c["src_spacing"], c["src_origin"])
+    z, d = Executor(precision=precision).measure_ncc(tgt, src, c["mats"], False)
+    assert _close(z, c["ncc_full"], RTOL[precision])[0]
+    assert np.array_equal(d, c["degen_full"])
+
+
+def _c1():
+    g = golden("smc.npz")
+    dims = tuple(int(x) for x in g["c1_dims"])
+    n = int(np.prod(dims))
+    t = np.unpackbits(g["c1_target_bits"])[:n].reshape(dims).astype(np.float64)
+    s = np.unpackbits(g["c1_source_bits"])[:n].reshape(dims).astype(np.float64)
+    return g, t, s
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64", "exact"])
+def test_c1_lockstep_iteration0(precision):
+    """C1 (64^3 masks, 500 particles): the reference's iteration-0 batch."""
+    g, t, s = _c1()
+    z, d, n = _measure(_vol(t, (1, 1, 1), (0, 0, 0)), _vol(s, (1, 1, 1), (0, 0, 0)),
+                       g["c1_a_it0"], g["c1_b_it0"], False, precision)
+    ok_, err = _close(z, g["c1_z"][0], RTOL[precision])
+    assert ok_, err
+    assert np.array_equal(d, g["c1_degen"][0])
+    # overlap counts against the bit-exact oracle
+    _, _, n_or = ok.ncc_measure_batch(t, s, g["c1_a_it0"], g["c1_b_it0"], True,
+                                      return_counts=True)
+    assert np.array_equal(n, n_or)
+
+
+def test_sharding_is_bitwise_invariant():
+    """Any split of the particle set gives bit-identical results (the
+    reference's worker-count invariance, tests/test_kernels.py:106-116)."""
+    g, t, s = _c1()
+    tv, sv = _vol(t, (1, 1, 1), (0, 0, 0)), _vol(s, (1, 1, 1), (0, 0, 0))
+    a, b = g["c1_a_it0"], g["c1_b_it0"]
+    full = _measure(tv, sv, a, b, False, "f64")[0]
+    for parts in (2, 3, 7):
+        cuts = np.linspace(0, a.shape[0], parts + 1).astype(int)
+        got = np.concatenate([_measure(tv, sv, a[lo:hi], b[lo:hi], False, "f64")[0]
+                              for lo, hi in zip(cuts[:-1], cuts[1:])])
+        assert np.array_equal(got, full)
+
+
+def test_identity_scores_one_and_out_of_frame_degenerate():
+    from paper_2504_19930_b200 import Executor, RigidParams, Volume3, to_matrix
+
+    rng = np.random.default_rng(3)
+    v = Volume3(rng.random((7, 7, 7), dtype=np.float32).astype(np.float64))
+    z, d = Executor().measure_ncc(v, v, np.eye(4)[np.newaxis])
+    assert z[0] == pytest.approx(1.0, abs=1e-12) and not d[0]
+    gone = to_matrix(RigidParams(tx=1e5))
+    z, d = Executor().measure_ncc(v, v, gone[np.newaxis])
+    assert z[0] == 0.0 and d[0]
+
+
+def _echo_pair(dims=(176, 176, 208), seed=0):
+    """uint8 echo-like pair on a C2-shaped grid (host construction, small cost)."""
+    rng = np.random.default_rng(seed)
+    nx, ny, nz = dims
+    x = (np.arange(nx) - nx / 2)[:, None, None] / (0.35 * nx)
+    y = (np.arange(ny) - ny / 2)[None, :, None] / (0.30 * ny)
+    z = (np.arange(nz) - nz / 2)[None, None, :] / (0.40 * nz)
+    r = x * x + y * y + z * z
+    base = np.where(r <= 1.0, 200.0, 40.0) * np.where(r <= 0.45, 0.2, 1.0)
+    speck = np.exp(0.3 * rng.standard_normal(dims))
+    raw = np.clip(np.round(base * speck), 0, 255)
+    raw2 = np.roll(raw, (2, -3, 1), axis=(0, 1, 2))
+    return raw, raw2
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_c2_shaped_uint8_codec_vs_oracle(precision):
+    """176x176x208 raw uint8 images, z-scored (codec path: 1-byte gathers with
+    the affine folded in) against the C oracle on the normalised fp64 data."""
+    from paper_2504_19930_b200 import Volume3, normalize_zscore
+    from paper_2504_19930_b200.geometry import index_affine_batch, to_matrix, RigidParams
+
+    raw_t, raw_s = _echo_pair()
+    sp = (0.87, 1.08, 0.73)
+    tv = normalize_zscore(Volume3(raw_t, sp))
+    sv = normalize_zscore(Volume3(raw_s, sp))
+    assert tv.codec is not None and sv.codec is not None
+    rng = np.random.default_rng(1)
+    mats = np.stack([to_matrix(RigidParams(*rng.uniform(-0.26, 0.26, 3),
+                                           *rng.uniform(-20, 20, 3)), tv.physical_center())
+                     for _ in range(12)])
+    a, b = index_affine_batch(mats, sp, (0, 0, 0), sp, (0, 0, 0))
+    for overlap in (False, True):
+        z, d, n = _measure(tv, sv, a, b, overlap, precision)
+        zo, do, no = ok.ncc_measure_batch(tv.data, sv.data, a, b, overlap, return_counts=True)
+        ok_, err = _close(z, zo, 1e-4 if precision == "f32" else 1e-9)
+        assert ok_, (overlap, err)
+        assert np.array_equal(d, do)
+        assert np.array_equal(n, no)
+
+
+def test_resample_bit_exact_vs_reference():
+    from paper_2504_19930_b200 import kernels_sm100
+
+    for name in ("cube10", "ragged", "flat", "mask12", "tiny_src"):
+        c = CASES[name]
+        for p in range(c["resampled"].shape[0]):
+            out = kernels_sm100.resample_trilinear(c["src"], c["a"][p], c["b"][p],
+                                                   c["tgt"].shape)
+            assert np.array_equal(out, c["resampled"][p]), (name, p)
+
+
+def test_kernel_module_seam_host_buffers():
+    from paper_2504_19930_b200 import kernels_sm100
+
+    c = CASES["ragged"]
+    z, d = kernels_sm100.ncc_measure_batch(c["tgt"], c["src"], c["a"], c["b"], True)
+    assert _close(z, c["ncc_overlap"], 1e-10)[0]
+    assert np.array_equal(d, c["degen_overlap"])
+    assert math.isfinite(float(z.sum()))
