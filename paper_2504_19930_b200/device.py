@@ -44,6 +44,8 @@ def require_cuda(device=None):
             "no CUDA device: the sm_100a path has no CPU fallback "
             "(run on a B200 via gpurun)")
     _lib.load()
+    if isinstance(device, t.device):
+        return device if device.index is not None else t.device("cuda", t.cuda.current_device())
     return t.device("cuda", t.cuda.current_device() if device is None else int(device))
 
 

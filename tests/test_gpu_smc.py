@@ -1,0 +1,266 @@
+"""Device SMC machinery and full registrations against the reference's
+recorded runs (tests/golden/smc.npz, produced by echoreg.register_smc).
+
+Tolerances (BASELINE north star): final transform within 0.1 degree and
+0.1 voxel; Dice within 1e-3; RNG-driven stages bit-exact.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from .conftest import golden
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+DEG_TOL = 0.1
+VOX_TOL = 0.1
+
+
+def _dev():
+    from paper_2504_19930_b200.device import require_cuda
+
+    return require_cuda()
+
+
+def test_init_bit_exact():
+    from paper_2504_19930_b200 import ops
+    from paper_2504_19930_b200.smc import SmcConfig
+
+    g = golden("rng.npz")
+    for seed, n in ((0, 500), (99, 7), (3, 2000)):
+        cfg = SmcConfig(n_particles=n, seed=seed)
+        st = ops.smc_init(n, seed, cfg.state_limits(), _dev()).cpu().numpy()
+        assert np.array_equal(st, g[f"init_{seed}_{n}"]), (seed, n)
+
+
+@pytest.mark.parametrize("seed,k", [(0, 0), (0, 3), (7, 19), (2**31 + 5, 1)])
+def test_predict_normals_bit_exact(seed, k):
+    from paper_2504_19930_b200 import ops
+
+    want = golden("rng.npz")[f"normals_{seed}_{k}"]
+    zero = torch.zeros((want.shape[0], 6), dtype=torch.float64, device=_dev())
+    out = torch.empty_like(zero)
+    ops.smc_predict(zero, out, seed, k, np.ones(6), np.full(6, 1e300))
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_predict_end_to_end_and_clamp():
+    from paper_2504_19930_b200.smc import ParticleSet, SmcConfig, predict
+
+    g = golden("rng.npz")
+    cfg = SmcConfig(n_particles=300, seed=4, sigma0_r=3.0, sigma0_t=4.0)
+    ps = ParticleSet(g["predict_in"], np.full(300, 1 / 300), np.zeros(300), 6, 4)
+    assert np.array_equal(predict(ps, cfg).states, g["predict_out"])
+    cfg2 = SmcConfig(n_particles=64, sigma0_t=500.0, sigma0_r=500.0, seed=1)
+    ps2 = ParticleSet(g["clamp_in"], np.full(64, 1 / 64), np.zeros(64), 0, 1)
+    assert np.array_equal(predict(ps2, cfg2).states, g["clamp_out"])
+
+
+def test_states_to_affine_matches_reference_geometry():
+    from paper_2504_19930_b200 import ops
+
+    g = golden("geometry.npz")
+    n = g["params"].shape[0]
+    st = torch.as_tensor(g["params"], device=_dev())
+    for i in range(0, n, 50):
+        A, B = ops.states_to_affine(st, i, 1, g["centers"][i],
+                                    (g["tgt_spacing"], g["tgt_origin"]),
+                                    (g["src_spacing"], g["src_origin"]))
+        np.testing.assert_allclose(A.cpu().numpy().reshape(3, 3), g["a"][i], rtol=0, atol=1e-13)
+        np.testing.assert_allclose(B.cpu().numpy().reshape(3), g["b"][i], rtol=1e-13, atol=1e-11)
+
+
+def _c1_volumes():
+    from paper_2504_19930_b200 import Volume3
+
+    g = golden("smc.npz")
+    dims = tuple(int(x) for x in g["c1_dims"])
+    n = int(np.prod(dims))
+    t = np.unpackbits(g["c1_target_bits"])[:n].reshape(dims).astype(np.float64)
+    s = np.unpackbits(g["c1_source_bits"])[:n].reshape(dims).astype(np.float64)
+    return g, Volume3(t), Volume3(s)
+
+
+def _assert_transform_close(got, want, spacing=(1.0, 1.0, 1.0)):
+    got, want = np.asarray(got), np.asarray(want)
+    drot = np.degrees(np.abs(got[:3] - want[:3]))
+    dvox = np.abs(got[3:] - want[3:]) / np.asarray(spacing)
+    assert np.all(drot <= DEG_TOL), drot
+    assert np.all(dvox <= VOX_TOL), dvox
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64", "exact"])
+def test_c1_full_registration_matches_reference(precision):
+    """BASELINE config 1: mask SMC, 64^3, 500 particles, 20 iterations."""
+    from paper_2504_19930_b200 import Executor, SmcConfig, register_smc
+
+    g, tm, sm = _c1_volumes()
+    cfg = SmcConfig(mode="mask", n_particles=500, n_iterations=20, seed=0)
+    est, trace = register_smc(tm, sm, cfg, Executor(precision=precision))
+    _assert_transform_close(est.to_array(), g["c1_estimate"])
+    np.testing.assert_allclose(trace.mean_measurement[0], g["c1_mean_measurement"][0],
+                               rtol=1e-4)
+    assert trace.resampled[:5] == list(g["c1_resampled"][:5])
+
+
+def test_c1_trace_lockstep_exact_mode():
+    """With fp64 sampling the whole trace follows the reference run."""
+    from paper_2504_19930_b200 import Executor, SmcConfig, register_smc
+
+    g, tm, sm = _c1_volumes()
+    cfg = SmcConfig(mode="mask", n_particles=500, n_iterations=20, seed=0)
+    est, trace = register_smc(tm, sm, cfg, Executor(precision="exact"))
+    assert trace.resampled == list(g["c1_resampled"])
+    np.testing.assert_allclose(trace.ess, g["c1_ess"], rtol=1e-6)
+    np.testing.assert_allclose(trace.max_measurement, g["c1_max_measurement"], rtol=1e-9)
+    np.testing.assert_allclose(trace.best_measurement, g["c1_best_measurement"], rtol=1e-9)
+    np.testing.assert_allclose(np.stack([e.to_array() for e in trace.estimates]),
+                               g["c1_estimates"], rtol=0, atol=1e-6)
+
+
+def test_c1_overlap_region_run():
+    from paper_2504_19930_b200 import Executor, SmcConfig, register_smc
+
+    g, tm, sm = _c1_volumes()
+    cfg = SmcConfig(mode="mask", n_particles=200, n_iterations=6, seed=3,
+                    ncc_region="overlap")
+    est, trace = register_smc(tm, sm, cfg, Executor(precision="exact"))
+    _assert_transform_close(est.to_array(), g["c1o_estimate"])
+    assert trace.resampled == list(g["c1o_resampled"])
+
+
+def test_image_mode_with_dice_trace():
+    from paper_2504_19930_b200 import Executor, SmcConfig, Volume3, register_smc
+
+    g = golden("smc.npz")
+    from paper_2504_19930_b200.volume import normalize_zscore  # noqa: F401
+
+    tv, sv = Volume3(g["img_target"]), Volume3(g["img_source"])
+    tmask = Volume3(g["img_target_mask"].astype(np.float64))
+    smask = Volume3(g["img_source_mask"].astype(np.float64))
+    cfg = SmcConfig(mode="image", n_particles=96, n_iterations=10, seed=2, t_limit=6.0,
+                    r_limit=8.0)
+    est, trace = register_smc(tv, sv, cfg, Executor(precision="exact"),
+                              trace_masks=(tmask, smask))
+    _assert_transform_close(est.to_array(), g["img_estimate"])
+    np.testing.assert_allclose(trace.dsc, g["img_dsc"], atol=1e-3)
+
+
+def test_sharded_update_equals_single_gpu_run():
+    """World-size invariance of the device loop: measuring the population in
+    shards (as N ranks would) and running the replicated update gives a
+    bit-identical trajectory."""
+    from paper_2504_19930_b200 import Executor, SmcConfig
+    from paper_2504_19930_b200 import dist, smc
+
+    g, tm, sm = _c1_volumes()
+    cfg = SmcConfig(mode="mask", n_particles=120, n_iterations=5, seed=7)
+    ref = smc.DeviceSmcRun(tm, sm, cfg, Executor())
+    for k in range(cfg.n_iterations):
+        ref.step(k)
+    base = ref.trace.cpu().numpy()
+    for world in (2, 3):
+        runs = [smc.DeviceSmcRun(tm, sm, cfg, Executor()) for _ in range(world)]
+        for r, run in enumerate(runs):
+            run.plan = dist.ShardPlan(cfg.n_particles, world, r)
+        # emulate the all-gather by stitching the shards measured by each "rank"
+        for k in range(cfg.n_iterations):
+            from paper_2504_19930_b200 import ops
+
+            zs = []
+            for run in runs:
+                pl = run.plan
+                ops.smc_predict(run.states, run.pred, cfg.seed, k, cfg.sigma_at(k), run.clip)
+                A, B = ops.states_to_affine(run.pred, pl.lo, pl.count, run.center, run.tgeom,
+                                            run.sgeom)
+                zs.append(ops.measure(run.tdv, run.sdv, A, B, False, "f64"))
+            z = torch.cat([x[0] for x in zs])
+            dg = torch.cat([x[1] for x in zs])
+            run0 = runs[0]
+            from paper_2504_19930_b200 import _lib
+            from paper_2504_19930_b200.device import ptr, stream_ptr
+
+            _lib.call("er_smc_update", ptr(z), ptr(dg), ptr(run0.weights), ptr(run0.pred),
+                      ptr(run0.states), ptr(run0.z_out), ptr(run0.scratch), run0.n,
+                      float(cfg.beta), float(cfg.ess_fraction), smc._u64(cfg.seed), k, 0,
+                      ptr(run0.ctl), ptr(run0.trace[k]), stream_ptr(run0.dev))
+            for run in runs[1:]:
+                run.states.copy_(run0.states)
+        assert np.array_equal(runs[0].trace.cpu().numpy(), base), world
+
+
+def test_exhaustive_matches_reference():
+    from paper_2504_19930_b200 import Executor, GridSpec, Volume3, register_exhaustive
+
+    g = golden("exhaustive.npz")
+    t, s = Volume3(g["target"]), Volume3(g["source"])
+    for name in ("g1", "g2"):
+        hc = tuple(int(x) for x in g[f"{name}_half_counts"])
+        step_t, step_r = (float(x) for x in g[f"{name}_steps"])
+        grid = GridSpec(half_counts=hc, step_t=step_t, step_r=step_r)
+        best, value = register_exhaustive(t, s, grid, Executor(precision="exact"))
+        assert np.array_equal(best.to_array(), g[f"{name}_best"]), name
+        assert float(value) == pytest.approx(float(g[f"{name}_value"]), rel=1e-10)
+
+
+def test_exhaustive_counting_executor_seam():
+    """Executor subclasses still see every node exactly once
+    (reference tests/test_exhaustive.py:109-120)."""
+    from paper_2504_19930_b200 import Executor, GridSpec, Volume3, register_exhaustive
+
+    g = golden("exhaustive.npz")
+    t, s = Volume3(g["target"]), Volume3(g["source"])
+
+    class Counting(Executor):
+        def measure_ncc(self, target, source, mats, overlap_only=False):
+            object.__setattr__(self, "calls", getattr(self, "calls", 0) + len(mats))
+            return super().measure_ncc(target, source, mats, overlap_only)
+
+    grid = GridSpec(half_counts=(1, 0, 1, 1, 0, 1), step_t=1.0, step_r=2.0)
+    ex = Counting()
+    register_exhaustive(t, s, grid, ex)
+    assert ex.calls == grid.n_nodes
+
+
+def test_phantom_port_matches_reference():
+    from paper_2504_19930_b200 import PhantomSpec, RigidParams, make_pair, make_phantom
+
+    g = golden("phantom.npz")
+    spec = PhantomSpec(dims=(20, 18, 22), spacing=(1.1, 0.9, 1.3), frames=3, seed=11,
+                       outer_semiaxes=(8.0, 7.0, 9.0), inner_semiaxes=(5.0, 4.0, 6.0))
+    seq, masks = make_phantom(spec)
+    assert np.array_equal(np.stack([f.data for f in seq.frames]), g["frames"])
+    truth = RigidParams(math.radians(6), math.radians(-3), math.radians(2), 1.5, -2.0, 0.5)
+    case = make_pair(seq, masks, truth, overlap_crop=0.2)
+    np.testing.assert_allclose(np.stack([f.data for f in case.source.frames]),
+                               g["src_frames"], rtol=0, atol=1e-12)
+    assert np.array_equal(np.stack([m.data for m in case.source_masks]).astype(np.uint8),
+                          g["src_masks"])
+    assert case.initial_dsc == pytest.approx(float(g["initial_dsc"]), abs=1e-12)
+
+
+def test_register_sequence_matches_reference():
+    from paper_2504_19930_b200 import (Executor, Sequence4, SmcConfig, Volume3,
+                                       register_sequence)
+
+    g = golden("pipeline.npz")
+    tgt = Sequence4([Volume3(f) for f in g["target"]])
+    src = Sequence4([Volume3(f) for f in g["source"]])
+    mt = [Volume3(m.astype(np.float64)) for m in g["target_masks"]]
+    ms = [Volume3(m.astype(np.float64)) for m in g["source_masks"]]
+    cfg = SmcConfig(mode="mask", n_particles=64, n_iterations=8, seed=1, t_limit=6.0,
+                    r_limit=8.0)
+    rep = register_sequence(tgt, src, mt, ms, cfg, Executor(precision="exact"))
+    est = np.array([rep.estimate_deg_mm[k] for k in
+                    ("rx_deg", "ry_deg", "rz_deg", "tx_mm", "ty_mm", "tz_mm")])
+    assert np.all(np.abs(est[:3] - g["estimate"][:3]) <= DEG_TOL)
+    assert np.all(np.abs(est[3:] - g["estimate"][3:]) <= VOX_TOL)
+    np.testing.assert_allclose(rep.ncc_before, g["ncc_before"], rtol=1e-9)
+    np.testing.assert_allclose(rep.ncc_after, g["ncc_after"], rtol=1e-6)
+    np.testing.assert_allclose(rep.dsc_before, g["dsc_before"], atol=1e-12)
+    np.testing.assert_allclose(rep.dsc_after, g["dsc_after"], atol=1e-3)
+    np.testing.assert_allclose(np.array(rep.trace["dsc"], dtype=float), g["trace_dsc"],
+                               atol=1e-3)
