@@ -1,0 +1,413 @@
+"""Benchmark: particle-voxel evals/s of the SMC registration hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): image-based SMC on a synthetic
+176x176x208 uint8 echo-like volume pair (the reference's LV phantom scaled to
+the echo grid, quantised to 8 bit, z-scored), 2000 particles, ED frame.
+A *step* is one device-resident SMC iteration over the whole particle set:
+predict (Philox/ziggurat) -> index affines -> fused gather+NCC measurement ->
+[NCCL all-gather of z when N > 1] -> weights/ESS/systematic resampling/
+estimate.  ``value`` = particle-voxel evaluations (P x voxels, the
+reference's full-region count) per second over all ranks, inputs resident.
+L2 is flushed (256 MiB write) between timed steps; each step is timed with
+CUDA events on the launching stream, max over ranks.
+
+``e2e``: the same metric through the public API -- one ``register_smc`` call
+per step (50 iterations, the reference default) on fresh volume objects, so
+every step uploads both volumes from pinned host memory and reads the trace
+back.  ``--impl reference`` times the reference algorithm on the host CPU
+(the bit-exact C restatement in oracle/, all host threads) on a bounded
+particle sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import copy
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-voxel evals/sec"
+UNIT = "evals/s"
+WORKLOAD = "C2: image-mode SMC, 176x176x208 uint8 echo-like pair, 2000 particles, ED frame"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--particles", type=int, default=2000)
+    ap.add_argument("--precision", default=None, help="f32 | f64 | exact")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-iters", type=int, default=50)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def make_workload():
+    """Deterministic C2 inputs (host): normalised Volume3 pair with uint8 codec."""
+    from paper_2504_19930_b200 import normalize_zscore
+    from paper_2504_19930_b200.phantom import echo_case
+
+    case = echo_case(frames=1, seed=0)
+    t = normalize_zscore(case.target.frames[0])
+    s = normalize_zscore(case.source.frames[0])
+    return t, s, case
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_rate(t, s, a, b, seconds, threads=0):
+    """Oracle (bit-exact C restatement of kernels_numba._ncc_kernel) on the
+    host cores over a bounded particle sample; returns (evals/s, sample, P, threads)."""
+    from oracle import kernels as ok
+
+    ok.build()
+    threads = threads or ok.max_threads()
+    nvox = t.data.size
+    p = max(threads, 8)
+    p = min(p, a.shape[0])
+    t0 = time.perf_counter()
+    ok.ncc_measure_batch(t.data, s.data, a[:p], b[:p], False, threads)
+    dt = time.perf_counter() - t0
+    # scale the sample so one timed pass is ~`seconds` of CPU work
+    want = int(p * max(1.0, seconds / max(dt, 1e-3)))
+    want = max(p, min(want, a.shape[0]))
+    reps = max(1, math.ceil(want / a.shape[0]))
+    idx = np.arange(want) % a.shape[0]
+    t0 = time.perf_counter()
+    ok.ncc_measure_batch(t.data, s.data, a[idx], b[idx], False, threads)
+    dt = time.perf_counter() - t0
+    del reps
+    return want * nvox / dt, want, dt, threads
+
+
+def first_iteration_affines(t, s, n, seed=0):
+    """Host copy of the particle set of SMC iteration 0 (init + predict, seed 0)."""
+    from paper_2504_19930_b200 import SmcConfig
+    from paper_2504_19930_b200.smc import ParticleSet, init_particles, predict
+    from paper_2504_19930_b200.geometry import index_affine_batch, to_matrix, RigidParams
+
+    cfg = SmcConfig(n_particles=n, seed=seed)
+    ps = predict(init_particles(cfg), cfg)
+    center = t.physical_center()
+    mats = np.stack([to_matrix(RigidParams.from_array(r), center) for r in ps.states])
+    return index_affine_batch(mats, s.spacing, s.origin, t.spacing, t.origin)
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    t, s, _ = make_workload()
+    from oracle import kernels as ok
+    from oracle.smc import Cfg, affines_for, init_states, predict
+
+    cfg = Cfg(n_particles=args.particles, seed=0)
+    st = predict(init_states(cfg), 0, cfg)
+    a, b = affines_for(st, (t.dims, t.spacing, t.origin), (s.dims, s.spacing, s.origin))
+    ok.build()
+    threads = ok.max_threads()
+    nvox = t.data.size
+    # bounded sample per step: one particle per thread x a small factor, so the
+    # whole --steps/--warmup run stays within a few minutes
+    p = min(a.shape[0], max(threads, 8) * 2)
+    t0 = time.perf_counter()
+    ok.ncc_measure_batch(t.data, s.data, a[:p], b[:p], False, threads)
+    one = time.perf_counter() - t0
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    p = max(threads, min(a.shape[0], int(p * budget / max(one, 1e-3))))
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        ok.ncc_measure_batch(t.data, s.data, a[:p], b[:p], False, threads)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = p * nvox / (ms * 1e-3)
+    sample = (f"ncc_measure_batch of the first {p} particles of SMC iteration 0 on the C2 "
+              f"176x176x208 pair (full region), {threads} threads, C oracle "
+              f"(bit-exact restatement of kernels_numba._ncc_kernel)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "particles_sampled": p, "voxels": nvox,
+                   "host_threads": threads},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+def measured_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        try:
+            with open(p) as fh:
+                d = json.load(fh)
+            return float(d["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        if rank == 0:
+            print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as td
+
+        td.init_process_group("nccl", device_id=dev)
+    from paper_2504_19930_b200 import Executor, SmcConfig, _lib, register_smc
+    from paper_2504_19930_b200 import smc as dsmc
+    from paper_2504_19930_b200.backend import Executor as _E  # noqa: F401
+
+    precision = args.precision or Executor().precision
+    ex = Executor(precision=precision, device=local)
+    t, s, _ = make_workload()
+    P = args.particles
+    cfg = SmcConfig(mode="image", n_particles=P, n_iterations=args.warmup + args.steps, seed=0)
+    run = dsmc.DeviceSmcRun(t, s, cfg, ex)
+    dsmc._check_inputs(run.tdv, run.sdv, cfg)
+    nvox = t.data.size
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for k in range(args.warmup):
+        run.step(k)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    mev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    n_in_sum = []
+    launches0 = _lib.launch_count
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush (outside the timed events)
+            k = args.warmup + i
+            ev[i][0].record(stream)
+            run.predict(k)
+            mev[i][0].record(stream)
+            run.measure()
+            mev[i][1].record(stream)
+            n_in_sum.append(run.n_local[: run.plan.count].sum())
+            run.update(k)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = _lib.launch_count - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    meas_ms = [a.elapsed_time(b) for a, b in mev]
+    total = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(total, op=torch.distributed.ReduceOp.MAX)
+    total_ms = float(total.item())
+    ms_per_step = total_ms / args.steps
+    value = P * nvox * args.steps / (total_ms * 1e-3)
+    sampled = float(sum(float(x.item()) for x in n_in_sum)) / max(1, len(n_in_sum))
+    meas_avg = sum(meas_ms) / max(1, len(meas_ms))
+    bytes_per_unit = 8 * run.sdv.storage.element_size() + run.tdv.storage.element_size()
+    peak, peak_kind = measured_peaks()
+    achieved_gbs = sampled * bytes_per_unit / (meas_avg * 1e-3) / 1e9
+    traffic = load_traffic()
+    roofline = {
+        "bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+        "frac": achieved_gbs / peak,
+        "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+        "kernel": "measure_partials_kernel (+finalize)",
+        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+        "bytes_per_sampled_voxel": bytes_per_unit,
+        "sampled_voxels_per_launch": sampled,
+        "kernel_ms": meas_avg,
+        "sampled_voxels_per_s": sampled / (meas_avg * 1e-3),
+        "kernel_share_of_step": meas_avg / ms_per_step,
+    }
+    clk = clocks.summary()
+
+    # ---- e2e through the public API: fresh volumes each step, pinned uploads
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e = run_e2e(args, t, s, ex, dev, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        a, b = first_iteration_affines(t, s, P)
+        rate, sample_p, secs, threads = cpu_reference_rate(t, s, a, b, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": (f"{sample_p} particles of SMC iteration 0 (C2 pair, full region) "
+                          f"through the C oracle (bit-exact restatement of "
+                          f"kernels_numba._ncc_kernel), {secs:.1f} s on {threads} host "
+                          f"threads")}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if precision == "f32" else "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "particles": P, "voxels": nvox,
+                       "volume_dims": list(t.dims), "storage": "u8 (raw echo, z-score folded)",
+                       "precision": precision, "l2": "flushed (256 MiB write) between steps",
+                       "step": "one device SMC iteration (predict+affine+measure+update)",
+                       "parallelism": f"particles sharded over {world} GPU(s)"},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_e2e(args, t, s, ex, dev, world):
+    """register_smc through the public API, fresh device copies every step."""
+    import torch
+
+    from paper_2504_19930_b200 import SmcConfig, register_smc
+
+    P = args.particles
+    cfg = SmcConfig(mode="image", n_particles=P, n_iterations=args.e2e_iters, seed=0)
+
+    def pinned_copy(v):
+        c = copy.copy(v)
+        if hasattr(c, "_er_device_cache"):
+            object.__delattr__(c, "_er_device_cache")
+        if v.codec is not None:
+            raw = torch.empty(v.codec.raw.shape, dtype=torch.uint8, pin_memory=True)
+            raw.numpy()[...] = v.codec.raw
+            object.__setattr__(c, "codec", type(v.codec)(raw.numpy(), v.codec.mean,
+                                                         v.codec.std))
+        return c
+
+    h2d = (t.codec.raw.nbytes + s.codec.raw.nbytes) if t.codec is not None else \
+        (t.data.nbytes + s.data.nbytes)
+    d2h = args.e2e_iters * 12 * 8 + 64
+    times = []
+    est = None
+    for i in range(1 + args.e2e_steps):  # first call is warm-up
+        tc, sc = pinned_copy(t), pinned_copy(s)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        est, _ = register_smc(tc, sc, cfg, ex)
+        torch.cuda.synchronize(dev)
+        el = time.perf_counter() - t0
+        if i > 0:
+            times.append(el)
+    tt = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    sec = float(tt.item()) / len(times)
+    evals = P * t.data.size * args.e2e_iters
+    return {"value": evals / sec, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": len(times),
+            "step": f"register_smc on fresh volumes, {args.e2e_iters} iterations",
+            "registration_ms_per_pair": sec * 1e3,
+            "estimate_deg_mm": [math.degrees(x) for x in est.to_array()[:3]]
+            + list(est.to_array()[3:])}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -45,6 +45,7 @@ typedef struct er_volume {
   int32_t dtype;        /* ER_U8 / ER_F32 / ER_F64 */
   int32_t nx, ny, nz;
   double alpha, gamma;  /* value = alpha * stored + gamma */
+  const void *oct_dev;  /* optional er_build_oct() re-layout of a u8 volume, or NULL */
 } er_volume;
 
 int er_abi_version(void);
@@ -58,6 +59,14 @@ const char *er_last_error(void);
  * doubles (the tail is reduction scratch). */
 #define ER_MOMENTS_DOUBLES 1026
 int er_volume_moments(const er_volume *v, double *out_dev, void *stream);
+
+/* Oct re-layout of a u8 volume for the measurement fast path: padded cell
+ * (ci, cj, ck) holds the 8 trilinear corners of floor cell (ci-1, cj-1, ck-1),
+ * clamped into the grid, as one 8-byte word.  er_oct_bytes() = (nx+1)(ny+1)
+ * (nz+1) * 8.  Set er_volume.oct_dev to the result to enable the fast path
+ * (used for lerp modes F32/F64; LERP_EXACT always gathers the plain copy). */
+size_t er_oct_bytes(const er_volume *v);
+int er_build_oct(const er_volume *v, void *oct_dev, void *stream);
 
 /* Classify an f64 device volume: flags_dev[0] = 1 if every voxel is 0 or 1
  * (volume.py:138-140), flags_dev[1] = 1 if every voxel is exactly

@@ -42,6 +42,7 @@ class ErVolume(ctypes.Structure):
         ("nz", _i32),
         ("alpha", _f64),
         ("gamma", _f64),
+        ("oct_dev", _p),
     ]
 
 
@@ -61,6 +62,8 @@ SIGNATURES = {
     "er_abi_version": (ctypes.c_int, []),
     "er_last_error": (ctypes.c_char_p, []),
     "er_volume_moments": (ctypes.c_int, [_VP, _p, _p]),
+    "er_oct_bytes": (ctypes.c_size_t, [_VP]),
+    "er_build_oct": (ctypes.c_int, [_VP, _p, _p]),
     "er_classify_f64": (ctypes.c_int, [_p, _i64, _p, _p]),
     "er_convert_f64": (ctypes.c_int, [_p, _i64, _i32, _p, _p]),
     "er_measure_workspace_bytes": (ctypes.c_size_t, [_VP, _i64]),
@@ -81,6 +84,15 @@ SIGNATURES = {
 }
 
 _lib = None
+
+#: kernels each entry point launches (for the bench's gpu_launches count)
+LAUNCHES_PER_CALL = {
+    "er_volume_moments": 2, "er_classify_f64": 2, "er_build_oct": 1, "er_convert_f64": 1, "er_measure_ncc": 2,
+    "er_smc_init": 1, "er_smc_predict": 1, "er_states_to_affine": 1, "er_grid_to_affine": 1,
+    "er_argmax_update": 1, "er_smc_update": 1, "er_resample": 1, "er_warp_dice_counts": 2,
+    "er_warp_ncc_sums": 4,
+}
+launch_count = 0
 
 
 def load():
@@ -110,8 +122,10 @@ def check(rc: int, what: str = ""):
 
 
 def call(name: str, *args):
+    global launch_count
     rc = getattr(load(), name)(*args)
     check(rc, name)
+    launch_count += LAUNCHES_PER_CALL.get(name, 0)
     return rc
 
 

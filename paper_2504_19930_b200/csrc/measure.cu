@@ -157,6 +157,45 @@ __device__ __forceinline__ double sample(const ST* __restrict__ src, double u, d
   }
 }
 
+// fixed-order block reduction of the per-thread sums -> one Partial per CTA
+__device__ __forceinline__ void block_write_partial(double sx, double sxx, double syx, double sy,
+                                                    double syy, long long cnt,
+                                                    Partial* __restrict__ part) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_down_sync(0xffffffffu, sx, o);
+    sxx += __shfl_down_sync(0xffffffffu, sxx, o);
+    syx += __shfl_down_sync(0xffffffffu, syx, o);
+    sy += __shfl_down_sync(0xffffffffu, sy, o);
+    syy += __shfl_down_sync(0xffffffffu, syy, o);
+    cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  }
+  __shared__ double red[kWarps][5];
+  __shared__ long long redn[kWarps];
+  if (lane == 0) {
+    red[warp][0] = sx;
+    red[warp][1] = sxx;
+    red[warp][2] = syx;
+    red[warp][3] = sy;
+    red[warp][4] = syy;
+    redn[warp] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Partial out{0.0, 0.0, 0.0, 0.0, 0.0, 0};
+    for (int w = 0; w < kWarps; ++w) {
+      out.x += red[w][0];
+      out.xx += red[w][1];
+      out.yx += red[w][2];
+      out.y += red[w][3];
+      out.yy += red[w][4];
+      out.n += redn[w];
+    }
+    part[blockIdx.x] = out;
+  }
+}
+
 template <typename TT, typename ST, int LERP>
 __global__ void __launch_bounds__(kThreads, 3)
     measure_partials_kernel(const TT* __restrict__ tgt, const ST* __restrict__ src,
@@ -227,38 +266,225 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
   }
 
-  // fixed-order block reduction
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    sx += __shfl_down_sync(0xffffffffu, sx, o);
-    sxx += __shfl_down_sync(0xffffffffu, sxx, o);
-    syx += __shfl_down_sync(0xffffffffu, syx, o);
-    sy += __shfl_down_sync(0xffffffffu, sy, o);
-    syy += __shfl_down_sync(0xffffffffu, syy, o);
-    cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  block_write_partial(sx, sxx, syx, sy, syy, cnt, part);
+}
+
+// ---------------------------------------------------------------------------
+// Fast path for 8-bit sources ("oct" layout).  The source is re-laid out once
+// per volume so that padded cell (ci, cj, ck) -- floor indices (ci-1, cj-1,
+// ck-1) -- holds its 8 trilinear corners in one 8-byte word, corners clamped
+// into the grid.  The one-cell pad ring reproduces the reference's clamped
+// edge cells (kernels_numba.py:32-55) without per-voxel clamps: a coordinate
+// epsilon below 0 or exactly at n-1 lands in a pad cell whose corners give
+// the same value.  Per sampled voxel: one LDG.64 for all 8 corners instead of
+// 8 byte gathers.  Source coordinates advance in exact Q24.40 fixed point
+// from the reference's fp64 row start (error <= 2^-41 (k+1) voxels); the
+// in-bounds k-run still comes from the bit-exact fp64 _k_interval.
+// ---------------------------------------------------------------------------
+
+constexpr double kFix = 1099511627776.0;  // 2^40
+
+__device__ __forceinline__ float byte_f32(unsigned w, unsigned sel) {
+  // float(byte) via the 2^23 magic: [b, 0, 0, 0x4B] - 2^23 (PRMT + FADD)
+  return __int_as_float(__byte_perm(w, 0x4B000000u, sel | 0x7650u)) - 8388608.0f;
+}
+
+__device__ __forceinline__ double byte_f64(unsigned w, unsigned sel) {
+  return __hiloint2double(0x43300000, __byte_perm(w, 0u, sel | 0x4440u)) - 4503599627370496.0;
+}
+
+__device__ __forceinline__ float frac_f32(long long q) {
+  // top 23 fraction bits -> [1, 2) - 1
+  const unsigned m = (unsigned)((unsigned long long)q >> 17) & 0x7FFFFFu;
+  return __int_as_float(0x3F800000u | m) - 1.0f;
+}
+
+__device__ __forceinline__ double frac_f64(long long q) {
+  const unsigned long long m = ((unsigned long long)q & 0xFFFFFFFFFFULL) << 12;
+  return __longlong_as_double(0x3FF0000000000000ULL | m) - 1.0;
+}
+
+template <typename TT>
+struct TgtAcc;  // per-row accumulation of target terms
+
+template <>
+struct TgtAcc<uint8_t> {  // exact integer sums of an 8-bit target
+  unsigned y = 0, yy = 0;
+  __device__ __forceinline__ float add(uint8_t v) {
+    y += v;
+    yy += (unsigned)v * v;
+    return (float)v;
   }
-  __shared__ double red[kWarps][5];
-  __shared__ long long redn[kWarps];
-  if (lane == 0) {
-    red[warp][0] = sx;
-    red[warp][1] = sxx;
-    red[warp][2] = syx;
-    red[warp][3] = sy;
-    red[warp][4] = syy;
-    redn[warp] = cnt;
+  __device__ __forceinline__ void fold(double& sy, double& syy) {
+    sy += (double)y;
+    syy += (double)yy;
+    y = yy = 0;
   }
+};
+
+template <typename TT>
+struct TgtAcc {
+  float y = 0.f, yy = 0.f;
+  __device__ __forceinline__ float add(TT v) {
+    const float f = (float)v;
+    y += f;
+    yy = fmaf(f, f, yy);
+    return f;
+  }
+  __device__ __forceinline__ void fold(double& sy, double& syy) {
+    sy += (double)y;
+    syy += (double)yy;
+    y = yy = 0.f;
+  }
+};
+
+struct OctGeom {
+  int cy, cz;  // padded cell counts along j and k (sy + 1, sz + 1)
+};
+
+template <typename TT, int LERP>
+__global__ void __launch_bounds__(kThreads, 3)
+    measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
+                       const double* __restrict__ A, const double* __restrict__ B, const Geom g,
+                       const OctGeom og, Partial* __restrict__ part) {
+  const int tile = blockIdx.x % g.ntiles;
+  const long long p = blockIdx.x / g.ntiles;
+  // the particle's affine lives in shared memory: it is only needed once per
+  // 32-row group, and keeping 12 doubles out of the registers of the inner
+  // loop is what lets this kernel run 3 CTAs/SM without spills
+  __shared__ double sab[12];
+  if (threadIdx.x < 12)
+    sab[threadIdx.x] = threadIdx.x < 9 ? A[9 * p + threadIdx.x] : B[3 * p + threadIdx.x - 9];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    Partial out{0.0, 0.0, 0.0, 0.0, 0.0, 0};
-    for (int w = 0; w < kWarps; ++w) {
-      out.x += red[w][0];
-      out.xx += red[w][1];
-      out.yx += red[w][2];
-      out.y += red[w][3];
-      out.yy += red[w][4];
-      out.n += redn[w];
+  // fixed-point per-k increments (exact integer stepping along the row)
+  const long long du = __double2ll_rn(sab[2] * kFix);
+  const long long dv = __double2ll_rn(sab[5] * kFix);
+  const long long dw = __double2ll_rn(sab[8] * kFix);
+
+  const int i_begin = tile * g.planes_per_tile;
+  const int i_end = min(g.nx, i_begin + g.planes_per_tile);
+  const int R = (i_end - i_begin) * g.ny;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  double sx = 0.0, sxx = 0.0, syx = 0.0, sy = 0.0, syy = 0.0;
+  int cnt = 0;
+  // the pad ring shifts every floor index by +1: fold it into the base pointer
+  const uint2* __restrict__ octb = oct + ((long long)og.cy + 1) * og.cz + 1;
+
+  for (int base = warp * 32; base < R; base += kThreads) {
+    const int r = base + lane;
+    int klo = 0, khi = 0, off = 0;
+    double u0 = 0.0, v0 = 0.0, w0 = 0.0;
+    if (r < R) {
+      const int i = i_begin + r / g.ny;
+      const int j = r - (r / g.ny) * g.ny;
+      const double di = (double)i, dj = (double)j;
+      u0 = rn_add(rn_add(rn_mul(sab[0], di), rn_mul(sab[1], dj)), sab[9]);
+      v0 = rn_add(rn_add(rn_mul(sab[3], di), rn_mul(sab[4], dj)), sab[10]);
+      w0 = rn_add(rn_add(rn_mul(sab[6], di), rn_mul(sab[7], dj)), sab[11]);
+      khi = g.nz;
+      k_interval(u0, sab[2], g.limx, klo, khi);
+      k_interval(v0, sab[5], g.limy, klo, khi);
+      k_interval(w0, sab[8], g.limz, klo, khi);
+      if (khi < klo) khi = klo;
+      off = (i * g.ny + j) * g.nz;
     }
-    part[blockIdx.x] = out;
+    cnt += khi - klo;
+    // row start in fixed point (per lane: its own row)
+    const long long fu0 = __double2ll_rn(u0 * kFix);
+    const long long fv0 = __double2ll_rn(v0 * kFix);
+    const long long fw0 = __double2ll_rn(w0 * kFix);
+    unsigned rows = __ballot_sync(0xffffffffu, khi > klo);
+    while (rows) {
+      const int q = __ffs(rows) - 1;
+      rows &= rows - 1;
+      const int qlo = __shfl_sync(0xffffffffu, klo, q);
+      const int qhi = __shfl_sync(0xffffffffu, khi, q);
+      const int qoff = __shfl_sync(0xffffffffu, off, q);
+      const int k0 = qlo + lane;
+      long long cu = __shfl_sync(0xffffffffu, fu0, q) + (long long)k0 * du;
+      long long cv = __shfl_sync(0xffffffffu, fv0, q) + (long long)k0 * dv;
+      long long cw = __shfl_sync(0xffffffffu, fw0, q) + (long long)k0 * dw;
+      TgtAcc<TT> ty;
+      float px = 0.f, pxx = 0.f, pyx = 0.f;     // fp32 row partials (LERP_F32)
+      double qx = 0.0, qxx = 0.0, qyx = 0.0;    // fp64 row partials (LERP_F64)
+      for (int k = k0; k < qhi; k += 32) {
+        const int ci = (int)(cu >> 40), cj = (int)(cv >> 40), ck = (int)(cw >> 40);
+        const uint2 c8 = __ldg(octb + ((long long)ci * og.cy + cj) * og.cz + ck);
+        const float yf = ty.add(__ldg(tgt + qoff + k));
+        if (LERP == ER_LERP_F32) {
+          const float fu = frac_f32(cu), fv = frac_f32(cv), fw = frac_f32(cw);
+          const float x000 = byte_f32(c8.x, 0), x100 = byte_f32(c8.x, 1);
+          const float x010 = byte_f32(c8.x, 2), x110 = byte_f32(c8.x, 3);
+          const float x001 = byte_f32(c8.y, 0), x101 = byte_f32(c8.y, 1);
+          const float x011 = byte_f32(c8.y, 2), x111 = byte_f32(c8.y, 3);
+          const float c00 = fmaf(fu, x100 - x000, x000);
+          const float c10 = fmaf(fu, x110 - x010, x010);
+          const float c01 = fmaf(fu, x101 - x001, x001);
+          const float c11 = fmaf(fu, x111 - x011, x011);
+          const float c0 = fmaf(fv, c10 - c00, c00);
+          const float c1 = fmaf(fv, c11 - c01, c01);
+          const float x = fmaf(fw, c1 - c0, c0);
+          px += x;
+          pxx = fmaf(x, x, pxx);
+          pyx = fmaf(yf, x, pyx);
+        } else {
+          const double fu = frac_f64(cu), fv = frac_f64(cv), fw = frac_f64(cw);
+          const double x000 = byte_f64(c8.x, 0), x100 = byte_f64(c8.x, 1);
+          const double x010 = byte_f64(c8.x, 2), x110 = byte_f64(c8.x, 3);
+          const double x001 = byte_f64(c8.y, 0), x101 = byte_f64(c8.y, 1);
+          const double x011 = byte_f64(c8.y, 2), x111 = byte_f64(c8.y, 3);
+          const double c00 = fma(fu, x100 - x000, x000);
+          const double c10 = fma(fu, x110 - x010, x010);
+          const double c01 = fma(fu, x101 - x001, x001);
+          const double c11 = fma(fu, x111 - x011, x011);
+          const double c0 = fma(fv, c10 - c00, c00);
+          const double c1 = fma(fv, c11 - c01, c01);
+          const double x = fma(fw, c1 - c0, c0);
+          qx += x;
+          qxx = fma(x, x, qxx);
+          qyx = fma((double)yf, x, qyx);
+        }
+        cu += 32 * du;
+        cv += 32 * dv;
+        cw += 32 * dw;
+      }
+      if (LERP == ER_LERP_F32) {
+        sx += (double)px;
+        sxx += (double)pxx;
+        syx += (double)pyx;
+      } else {
+        sx += qx;
+        sxx += qxx;
+        syx += qyx;
+      }
+      ty.fold(sy, syy);
+    }
+  }
+  block_write_partial(sx, sxx, syx, sy, syy, cnt, part);
+}
+
+// Oct re-layout of an 8-bit source (one thread per padded cell).
+__global__ void build_oct_kernel(const uint8_t* __restrict__ s, int sx, int sy, int sz,
+                                 uint2* __restrict__ oct) {
+  const int cx = sx + 1, cy = sy + 1, cz = sz + 1;
+  const long long n = (long long)cx * cy * cz;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int ck = (int)(q % cz);
+    const long long rest = q / cz;
+    const int cj = (int)(rest % cy);
+    const int ci = (int)(rest / cy);
+    const int i0 = min(max(ci - 1, 0), sx - 1), i1 = min(ci, sx - 1);
+    const int j0 = min(max(cj - 1, 0), sy - 1), j1 = min(cj, sy - 1);
+    const int k0 = min(max(ck - 1, 0), sz - 1), k1 = min(ck, sz - 1);
+    auto at = [&](int i, int j, int k) -> unsigned {
+      return s[((long long)i * sy + j) * sz + k];
+    };
+    uint2 w;
+    w.x = at(i0, j0, k0) | (at(i1, j0, k0) << 8) | (at(i0, j1, k0) << 16) | (at(i1, j1, k0) << 24);
+    w.y = at(i0, j0, k1) | (at(i1, j0, k1) << 8) | (at(i0, j1, k1) << 16) | (at(i1, j1, k1) << 24);
+    oct[q] = w;
   }
 }
 
@@ -403,10 +629,26 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
     return er_set_error(ER_EINVAL, "er_measure_ncc: too many particles for one launch");
   cudaStream_t st = as_stream(stream);
   Partial* part = (Partial*)workspace_dev;
-  switch (tgt->dtype) {
-    case ER_U8: launch_src<uint8_t>(lerp_mode, tgt, src, A_dev, b_dev, g, part, P, st); break;
-    case ER_F32: launch_src<float>(lerp_mode, tgt, src, A_dev, b_dev, g, part, P, st); break;
-    default: launch_src<double>(lerp_mode, tgt, src, A_dev, b_dev, g, part, P, st); break;
+  const bool use_oct = src->oct_dev && src->dtype == ER_U8 && lerp_mode != ER_LERP_EXACT;
+  if (use_oct) {
+    const OctGeom og{src->ny + 1, src->nz + 1};
+    const unsigned blocks = (unsigned)(P * g.ntiles);
+    const uint2* oct = (const uint2*)src->oct_dev;
+#define ER_OCT(TT, L) \
+  measure_oct_kernel<TT, L><<<blocks, kThreads, 0, st>>>((const TT*)tgt->data_dev, oct, A_dev, b_dev, g, og, part)
+    const bool f32 = lerp_mode == ER_LERP_F32;
+    switch (tgt->dtype) {
+      case ER_U8: if (f32) ER_OCT(uint8_t, ER_LERP_F32); else ER_OCT(uint8_t, ER_LERP_F64); break;
+      case ER_F32: if (f32) ER_OCT(float, ER_LERP_F32); else ER_OCT(float, ER_LERP_F64); break;
+      default: if (f32) ER_OCT(double, ER_LERP_F32); else ER_OCT(double, ER_LERP_F64); break;
+    }
+#undef ER_OCT
+  } else {
+    switch (tgt->dtype) {
+      case ER_U8: launch_src<uint8_t>(lerp_mode, tgt, src, A_dev, b_dev, g, part, P, st); break;
+      case ER_F32: launch_src<float>(lerp_mode, tgt, src, A_dev, b_dev, g, part, P, st); break;
+      default: launch_src<double>(lerp_mode, tgt, src, A_dev, b_dev, g, part, P, st); break;
+    }
   }
   ER_CHECK_LAUNCH();
   Affines f{src->alpha, src->gamma, tgt->alpha, tgt->gamma};
@@ -415,6 +657,23 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
   measure_finalize_kernel<<<(unsigned)((P + fb - 1) / fb), fb, 0, st>>>(
       part, g.ntiles, P, tgt_moments_dev, nvox, overlap_only ? 1 : 0, f, ncc_dev, degen_dev,
       n_in_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" size_t er_oct_bytes(const er_volume* v) {
+  if (!v || v->nx < 1 || v->ny < 1 || v->nz < 1) return 0;
+  return (size_t)(v->nx + 1) * (size_t)(v->ny + 1) * (size_t)(v->nz + 1) * sizeof(uint2);
+}
+
+extern "C" int er_build_oct(const er_volume* v, void* oct_dev, void* stream) {
+  if (!valid_volume(v) || v->dtype != ER_U8 || !oct_dev)
+    return er_set_error(ER_EINVAL, "er_build_oct: needs a u8 volume and an output buffer");
+  const long long n = (long long)(v->nx + 1) * (v->ny + 1) * (v->nz + 1);
+  long long blocks = (n + 255) / 256;
+  if (blocks > ER_NUM_SMS_B200 * 16) blocks = ER_NUM_SMS_B200 * 16;
+  build_oct_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+      (const uint8_t*)v->data_dev, v->nx, v->ny, v->nz, (uint2*)oct_dev);
   ER_CHECK_LAUNCH();
   return ER_OK;
 }

@@ -82,6 +82,18 @@ class DeviceVolume:
     def nbytes(self) -> int:
         return int(self.storage.numel() * self.storage.element_size())
 
+    def ensure_oct(self):
+        """Build (once) the oct re-layout of a u8 volume used as a measurement
+        source: all 8 trilinear corners of a cell in one 8-byte word."""
+        if self.dtype_code != _lib.ER_U8 or self.desc.oct_dev:
+            return
+        t = torch()
+        nbytes = int(_lib.load().er_oct_bytes(ctypes.byref(self.desc)))
+        self.oct = t.empty(nbytes, dtype=t.uint8, device=self.storage.device)
+        _lib.call("er_build_oct", ctypes.byref(self.desc), ptr(self.oct),
+                  stream_ptr(self.storage.device))
+        self.desc.oct_dev = self.oct.data_ptr()
+
 
 def _make_desc(storage, code, dims, alpha, gamma):
     d = _lib.ErVolume()

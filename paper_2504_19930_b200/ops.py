@@ -38,6 +38,8 @@ def measure(tdv: DeviceVolume, sdv: DeviceVolume, A, B, overlap: bool, precision
     ncc, degen, n_in = out
     if P == 0:
         return ncc, degen, n_in
+    if precision != "exact":
+        sdv.ensure_oct()
     need = _lib.load().er_measure_workspace_bytes(tdv.desc_ptr, P)
     ws = WORKSPACE.get(dev, need)
     _lib.call("er_measure_ncc", tdv.desc_ptr, sdv.desc_ptr, ptr(tdv.moments), ptr(A), ptr(B),
