@@ -282,27 +282,39 @@ __global__ void __launch_bounds__(kThreads, 3)
 // in-bounds k-run still comes from the bit-exact fp64 _k_interval.
 // ---------------------------------------------------------------------------
 
-constexpr double kFix = 1099511627776.0;  // 2^40
+// 2^23 + byte as an exact float: PRMT [b, 0, 0, 0x4B]
+__device__ __forceinline__ float byte_magic(unsigned w, unsigned sel) {
+  return __int_as_float(__byte_perm(w, 0x4B000000u, sel | 0x7650u));
+}
 
-__device__ __forceinline__ float byte_f32(unsigned w, unsigned sel) {
-  // float(byte) via the 2^23 magic: [b, 0, 0, 0x4B] - 2^23 (PRMT + FADD)
-  return __int_as_float(__byte_perm(w, 0x4B000000u, sel | 0x7650u)) - 8388608.0f;
+// lerp between two bytes of a word: a + f (b - a) with (b - a) formed exactly
+// on the 2^23-offset floats (one FADD fewer than converting both bytes)
+__device__ __forceinline__ float lerp_bytes(unsigned w, unsigned sa, unsigned sb, float f) {
+  const float A = byte_magic(w, sa), B = byte_magic(w, sb);
+  return fmaf(f, B - A, A - 8388608.0f);
 }
 
 __device__ __forceinline__ double byte_f64(unsigned w, unsigned sel) {
   return __hiloint2double(0x43300000, __byte_perm(w, 0u, sel | 0x4440u)) - 4503599627370496.0;
 }
 
-__device__ __forceinline__ float frac_f32(long long q) {
-  // top 23 fraction bits -> [1, 2) - 1
-  const unsigned m = (unsigned)((unsigned long long)q >> 17) & 0x7FFFFFu;
-  return __int_as_float(0x3F800000u | m) - 1.0f;
-}
-
-__device__ __forceinline__ double frac_f64(long long q) {
-  const unsigned long long m = ((unsigned long long)q & 0xFFFFFFFFFFULL) << 12;
-  return __longlong_as_double(0x3FF0000000000000ULL | m) - 1.0;
-}
+// Fixed-point source coordinates with FB fractional bits.  FB = 32 (fp32
+// lerps): the integer part is the high register, the fraction the low one.
+// FB = 40 (fp64 lerps): 40-bit fractions, error <= 2^-41 (k+1) voxels.
+template <int FB>
+struct Fix {
+  static constexpr double kScale = (double)(1ULL << FB);
+  __device__ __forceinline__ static int ipart(long long q) { return (int)(q >> FB); }
+  __device__ __forceinline__ static float frac32(long long q) {
+    // top 23 fraction bits -> [1, 2) - 1
+    const unsigned m = (unsigned)((unsigned long long)q >> (FB - 23)) & 0x7FFFFFu;
+    return __int_as_float(0x3F800000u | m) - 1.0f;
+  }
+  __device__ __forceinline__ static double frac64(long long q) {
+    const unsigned long long m = ((unsigned long long)q << (64 - FB)) >> 12;
+    return __longlong_as_double(0x3FF0000000000000ULL | m) - 1.0;
+  }
+};
 
 template <typename TT>
 struct TgtAcc;  // per-row accumulation of target terms
@@ -347,6 +359,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
                        const OctGeom og, Partial* __restrict__ part) {
+  using F = Fix<LERP == ER_LERP_F32 ? 32 : 40>;
   const int tile = blockIdx.x % g.ntiles;
   const long long p = blockIdx.x / g.ntiles;
   // the particle's affine lives in shared memory: it is only needed once per
@@ -357,19 +370,20 @@ __global__ void __launch_bounds__(kThreads, 3)
     sab[threadIdx.x] = threadIdx.x < 9 ? A[9 * p + threadIdx.x] : B[3 * p + threadIdx.x - 9];
   __syncthreads();
   // fixed-point per-k increments (exact integer stepping along the row)
-  const long long du = __double2ll_rn(sab[2] * kFix);
-  const long long dv = __double2ll_rn(sab[5] * kFix);
-  const long long dw = __double2ll_rn(sab[8] * kFix);
+  const long long du = __double2ll_rn(sab[2] * F::kScale);
+  const long long dv = __double2ll_rn(sab[5] * F::kScale);
+  const long long dw = __double2ll_rn(sab[8] * F::kScale);
 
   const int i_begin = tile * g.planes_per_tile;
   const int i_end = min(g.nx, i_begin + g.planes_per_tile);
   const int R = (i_end - i_begin) * g.ny;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cyz = og.cy * og.cz;
 
   double sx = 0.0, sxx = 0.0, syx = 0.0, sy = 0.0, syy = 0.0;
   int cnt = 0;
   // the pad ring shifts every floor index by +1: fold it into the base pointer
-  const uint2* __restrict__ octb = oct + ((long long)og.cy + 1) * og.cz + 1;
+  const uint2* __restrict__ octb = oct + (cyz + og.cz + 1);
 
   for (int base = warp * 32; base < R; base += kThreads) {
     const int r = base + lane;
@@ -391,17 +405,17 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
     cnt += khi - klo;
     // row start in fixed point (per lane: its own row)
-    const long long fu0 = __double2ll_rn(u0 * kFix);
-    const long long fv0 = __double2ll_rn(v0 * kFix);
-    const long long fw0 = __double2ll_rn(w0 * kFix);
+    const long long fu0 = __double2ll_rn(u0 * F::kScale);
+    const long long fv0 = __double2ll_rn(v0 * F::kScale);
+    const long long fw0 = __double2ll_rn(w0 * F::kScale);
     unsigned rows = __ballot_sync(0xffffffffu, khi > klo);
     while (rows) {
       const int q = __ffs(rows) - 1;
       rows &= rows - 1;
       const int qlo = __shfl_sync(0xffffffffu, klo, q);
       const int qhi = __shfl_sync(0xffffffffu, khi, q);
-      const int qoff = __shfl_sync(0xffffffffu, off, q);
       const int k0 = qlo + lane;
+      const TT* __restrict__ trow = tgt + __shfl_sync(0xffffffffu, off, q);
       long long cu = __shfl_sync(0xffffffffu, fu0, q) + (long long)k0 * du;
       long long cv = __shfl_sync(0xffffffffu, fv0, q) + (long long)k0 * dv;
       long long cw = __shfl_sync(0xffffffffu, fw0, q) + (long long)k0 * dw;
@@ -409,19 +423,16 @@ __global__ void __launch_bounds__(kThreads, 3)
       float px = 0.f, pxx = 0.f, pyx = 0.f;     // fp32 row partials (LERP_F32)
       double qx = 0.0, qxx = 0.0, qyx = 0.0;    // fp64 row partials (LERP_F64)
       for (int k = k0; k < qhi; k += 32) {
-        const int ci = (int)(cu >> 40), cj = (int)(cv >> 40), ck = (int)(cw >> 40);
-        const uint2 c8 = __ldg(octb + ((long long)ci * og.cy + cj) * og.cz + ck);
-        const float yf = ty.add(__ldg(tgt + qoff + k));
+        // 32-bit cell index: the padded grid has < 2^31 cells
+        const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
+        const uint2 c8 = __ldg(octb + cell);
+        const float yf = ty.add(__ldg(trow + k));
         if (LERP == ER_LERP_F32) {
-          const float fu = frac_f32(cu), fv = frac_f32(cv), fw = frac_f32(cw);
-          const float x000 = byte_f32(c8.x, 0), x100 = byte_f32(c8.x, 1);
-          const float x010 = byte_f32(c8.x, 2), x110 = byte_f32(c8.x, 3);
-          const float x001 = byte_f32(c8.y, 0), x101 = byte_f32(c8.y, 1);
-          const float x011 = byte_f32(c8.y, 2), x111 = byte_f32(c8.y, 3);
-          const float c00 = fmaf(fu, x100 - x000, x000);
-          const float c10 = fmaf(fu, x110 - x010, x010);
-          const float c01 = fmaf(fu, x101 - x001, x001);
-          const float c11 = fmaf(fu, x111 - x011, x011);
+          const float fu = F::frac32(cu), fv = F::frac32(cv), fw = F::frac32(cw);
+          const float c00 = lerp_bytes(c8.x, 0, 1, fu);
+          const float c10 = lerp_bytes(c8.x, 2, 3, fu);
+          const float c01 = lerp_bytes(c8.y, 0, 1, fu);
+          const float c11 = lerp_bytes(c8.y, 2, 3, fu);
           const float c0 = fmaf(fv, c10 - c00, c00);
           const float c1 = fmaf(fv, c11 - c01, c01);
           const float x = fmaf(fw, c1 - c0, c0);
@@ -429,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 3)
           pxx = fmaf(x, x, pxx);
           pyx = fmaf(yf, x, pyx);
         } else {
-          const double fu = frac_f64(cu), fv = frac_f64(cv), fw = frac_f64(cw);
+          const double fu = F::frac64(cu), fv = F::frac64(cv), fw = F::frac64(cw);
           const double x000 = byte_f64(c8.x, 0), x100 = byte_f64(c8.x, 1);
           const double x010 = byte_f64(c8.x, 2), x110 = byte_f64(c8.x, 3);
           const double x001 = byte_f64(c8.y, 0), x101 = byte_f64(c8.y, 1);

@@ -20,7 +20,7 @@ from .device import device_volume_from_array, require_cuda, torch
 NAME = "sm100"
 
 #: interpolation arithmetic used through this seam (precision)
-PRECISION = "f64"
+PRECISION = "f32"
 
 
 def ncc_measure_batch(tgt, src, a_batch, b_batch, overlap_only, workers=1):

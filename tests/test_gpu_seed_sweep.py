@@ -1,0 +1,75 @@
+"""Free-running end-to-end parity over many seeds.
+
+The SMC trajectory is chaotic in the likelihoods,
+so per-particle accuracy alone does not guarantee the final transform: this
+sweep runs complete registrations through the device path and through the
+reference algorithm (the numpy restatement in oracle/smc.py driving the
+bit-exact C kernel, pinned to the real reference by tests/test_oracle.py)
+and requires the final estimates to agree within 0.1 degree / 0.1 voxel for
+every seed and precision mode.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import smc as osmc
+
+from .conftest import golden
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+SEEDS = list(range(8))
+
+
+def _c1():
+    from paper_2504_19930_b200 import Volume3
+
+    g = golden("smc.npz")
+    dims = tuple(int(x) for x in g["c1_dims"])
+    n = int(np.prod(dims))
+    t = np.unpackbits(g["c1_target_bits"])[:n].reshape(dims).astype(np.float64)
+    s = np.unpackbits(g["c1_source_bits"])[:n].reshape(dims).astype(np.float64)
+    return Volume3(t), Volume3(s)
+
+
+def _img():
+    from paper_2504_19930_b200 import Volume3
+
+    g = golden("smc.npz")
+    return Volume3(g["img_target"]), Volume3(g["img_source"])
+
+
+def _sweep(tv, sv, mode, n, iters, precision, t_limit=20.0, r_limit=15.0):
+    from paper_2504_19930_b200 import Executor, SmcConfig, register_smc
+
+    worst_deg, worst_vox = 0.0, 0.0
+    geom_t = (tv.dims, tv.spacing, tv.origin)
+    geom_s = (sv.dims, sv.spacing, sv.origin)
+    for seed in SEEDS:
+        cfg = SmcConfig(mode=mode, n_particles=n, n_iterations=iters, seed=seed,
+                        t_limit=t_limit, r_limit=r_limit)
+        est, _ = register_smc(tv, sv, cfg, Executor(precision=precision))
+        ocfg = osmc.Cfg(mode=mode, n_particles=n, n_iterations=iters, seed=seed,
+                        t_limit=t_limit, r_limit=r_limit)
+        oest, _ = osmc.register(tv.data, sv.data, geom_t, geom_s, ocfg)
+        d = est.to_array() - oest
+        worst_deg = max(worst_deg, float(np.degrees(np.abs(d[:3])).max()))
+        worst_vox = max(worst_vox, float((np.abs(d[3:]) / np.asarray(tv.spacing)).max()))
+    return worst_deg, worst_vox
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64", "exact"])
+def test_c1_mask_seed_sweep(precision):
+    tv, sv = _c1()
+    deg, vox = _sweep(tv, sv, "mask", 500, 20, precision)
+    print(f"C1 mask {precision}: worst |d rot| {deg:.3g} deg, |d trans| {vox:.3g} vox")
+    assert deg <= 0.1 and vox <= 0.1
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64", "exact"])
+def test_image_mode_seed_sweep(precision):
+    tv, sv = _img()
+    deg, vox = _sweep(tv, sv, "image", 96, 10, precision, t_limit=6.0, r_limit=8.0)
+    print(f"img {precision}: worst |d rot| {deg:.3g} deg, |d trans| {vox:.3g} vox")
+    assert deg <= 0.1 and vox <= 0.1

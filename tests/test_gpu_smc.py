@@ -176,7 +176,7 @@ def test_sharded_update_equals_single_gpu_run():
                 ops.smc_predict(run.states, run.pred, cfg.seed, k, cfg.sigma_at(k), run.clip)
                 A, B = ops.states_to_affine(run.pred, pl.lo, pl.count, run.center, run.tgeom,
                                             run.sgeom)
-                zs.append(ops.measure(run.tdv, run.sdv, A, B, False, "f64"))
+                zs.append(ops.measure(run.tdv, run.sdv, A, B, False, run.ex.precision))
             z = torch.cat([x[0] for x in zs])
             dg = torch.cat([x[1] for x in zs])
             run0 = runs[0]
