@@ -382,8 +382,6 @@ __global__ void __launch_bounds__(kThreads, 3)
 
   double sx = 0.0, sxx = 0.0, syx = 0.0, sy = 0.0, syy = 0.0;
   int cnt = 0;
-  // the pad ring shifts every floor index by +1: fold it into the base pointer
-  const uint2* __restrict__ octb = oct + (cyz + og.cz + 1);
 
   for (int base = warp * 32; base < R; base += kThreads) {
     const int r = base + lane;
@@ -405,9 +403,12 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
     cnt += khi - klo;
     // row start in fixed point (per lane: its own row)
-    const long long fu0 = __double2ll_rn(u0 * F::kScale);
-    const long long fv0 = __double2ll_rn(v0 * F::kScale);
-    const long long fw0 = __double2ll_rn(w0 * F::kScale);
+    // (the +1.0 voxel shift to the padded cell index is an exact integer add,
+    // so the cell index below is a plain non-negative 32-bit IMAD chain)
+    const long long one = 1LL << (LERP == ER_LERP_F32 ? 32 : 40);
+    const long long fu0 = __double2ll_rn(u0 * F::kScale) + one;
+    const long long fv0 = __double2ll_rn(v0 * F::kScale) + one;
+    const long long fw0 = __double2ll_rn(w0 * F::kScale) + one;
     unsigned rows = __ballot_sync(0xffffffffu, khi > klo);
     while (rows) {
       const int q = __ffs(rows) - 1;
@@ -425,19 +426,31 @@ __global__ void __launch_bounds__(kThreads, 3)
       for (int k = k0; k < qhi; k += 32) {
         // 32-bit cell index: the padded grid has < 2^31 cells
         const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
-        const uint2 c8 = __ldg(octb + cell);
+        const uint2 c8 = __ldg(oct + (unsigned)cell);
         const float yf = ty.add(__ldg(trow + k));
         if (LERP == ER_LERP_F32) {
           const float fu = F::frac32(cu), fv = F::frac32(cv), fw = F::frac32(cw);
-          const float c00 = lerp_bytes(c8.x, 0, 1, fu);
-          const float c10 = lerp_bytes(c8.x, 2, 3, fu);
-          const float c01 = lerp_bytes(c8.y, 0, 1, fu);
-          const float c11 = lerp_bytes(c8.y, 2, 3, fu);
-          const float c0 = fmaf(fv, c10 - c00, c00);
-          const float c1 = fmaf(fv, c11 - c01, c01);
-          const float x = fmaf(fw, c1 - c0, c0);
-          px += x;
-          pxx = fmaf(x, x, pxx);
+          // packed fp32x2 (FFMA2/FADD2): corners paired along k so the u-lerps
+          // yield (c00, c01) and (c10, c11) and the v-lerp runs packed too
+          const float2 P0 = make_float2(byte_magic(c8.x, 0), byte_magic(c8.y, 0));
+          const float2 P1 = make_float2(byte_magic(c8.x, 1), byte_magic(c8.y, 1));
+          const float2 Q0 = make_float2(byte_magic(c8.x, 2), byte_magic(c8.y, 2));
+          const float2 Q1 = make_float2(byte_magic(c8.x, 3), byte_magic(c8.y, 3));
+          const float2 off2 = make_float2(-8388608.0f, -8388608.0f);
+          const float2 fu2 = make_float2(fu, fu), fv2 = make_float2(fv, fv);
+          // differences of the 2^23-offset floats are exact; so is removing the offset
+          const float2 cP = __ffma2_rn(fu2, __fadd2_rn(P1, make_float2(-P0.x, -P0.y)),
+                                       __fadd2_rn(P0, off2));   // (c00, c01)
+          const float2 cQ = __ffma2_rn(fu2, __fadd2_rn(Q1, make_float2(-Q0.x, -Q0.y)),
+                                       __fadd2_rn(Q0, off2));   // (c10, c11)
+          const float2 c = __ffma2_rn(fv2, __fadd2_rn(cQ, make_float2(-cP.x, -cP.y)),
+                                      cP);                      // (c0, c1)
+          const float x = fmaf(fw, c.y - c.x, c.x);
+          // (sum x, sum x^2) in one packed FMA
+          const float2 acc = __ffma2_rn(make_float2(x, x), make_float2(1.0f, x),
+                                        make_float2(px, pxx));
+          px = acc.x;
+          pxx = acc.y;
           pyx = fmaf(yf, x, pyx);
         } else {
           const double fu = F::frac64(cu), fv = F::frac64(cv), fw = F::frac64(cw);
