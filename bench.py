@@ -293,6 +293,8 @@ def run_ours(args):
     launches = _lib.launch_count - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     meas_ms = [a.elapsed_time(b) for a, b in mev]
+    pre_ms = [a[0].elapsed_time(b[0]) for a, b in zip(ev, mev)]
+    post_ms = [a[1].elapsed_time(b[1]) for a, b in zip(mev, ev)]
     total = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(total, op=torch.distributed.ReduceOp.MAX)
@@ -316,6 +318,8 @@ def run_ours(args):
         "kernel_ms": meas_avg,
         "sampled_voxels_per_s": sampled / (meas_avg * 1e-3),
         "kernel_share_of_step": meas_avg / ms_per_step,
+        "pre_ms_per_step": sum(pre_ms) / len(pre_ms),
+        "post_ms_per_step": sum(post_ms) / len(post_ms),
     }
     clk = clocks.summary()
 

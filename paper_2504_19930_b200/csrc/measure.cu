@@ -380,11 +380,19 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? 4 : 3)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cyz = og.cy * og.cz;
 
-  double sx = 0.0, sxx = 0.0, syx = 0.0, sy = 0.0, syy = 0.0;
+  // 32-row groups are handed out dynamically (warps whose rows are short or
+  // out of bounds take more groups); each group's warp-reduced sums land in
+  // the group's own shared slot and the slots are summed in group order, so
+  // the result does not depend on which warp ran which group.
+  __shared__ double gsum[kRowsPerTile / 32][5];
+  __shared__ int next_group;
+  const int ngroups = (R + 31) / 32;  // <= kRowsPerTile / 32 (make_geom)
+  if (threadIdx.x == 0) next_group = kWarps;
+  __syncthreads();
   int cnt = 0;
 
-  for (int base = warp * 32; base < R; base += kThreads) {
-    const int r = base + lane;
+  for (int grp = warp; grp < ngroups;) {
+    const int r = grp * 32 + lane;
     int klo = 0, khi = 0, off = 0;
     double u0 = 0.0, v0 = 0.0, w0 = 0.0;
     if (r < R) {
@@ -402,6 +410,10 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? 4 : 3)
       off = (i * g.ny + j) * g.nz;
     }
     cnt += khi - klo;
+    // per-lane group partials: fp32 (LERP_F32) or fp64, exact ints for u8 targets
+    TgtAcc<TT> ty;
+    float px = 0.f, pxx = 0.f, pyx = 0.f;
+    double qx = 0.0, qxx = 0.0, qyx = 0.0;
     // row start in fixed point (per lane: its own row)
     // (the +1.0 voxel shift to the padded cell index is an exact integer add,
     // so the cell index below is a plain non-negative 32-bit IMAD chain)
@@ -420,9 +432,6 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? 4 : 3)
       long long cu = __shfl_sync(0xffffffffu, fu0, q) + (long long)k0 * du;
       long long cv = __shfl_sync(0xffffffffu, fv0, q) + (long long)k0 * dv;
       long long cw = __shfl_sync(0xffffffffu, fw0, q) + (long long)k0 * dw;
-      TgtAcc<TT> ty;
-      float px = 0.f, pxx = 0.f, pyx = 0.f;     // fp32 row partials (LERP_F32)
-      double qx = 0.0, qxx = 0.0, qyx = 0.0;    // fp64 row partials (LERP_F64)
       for (int k = k0; k < qhi; k += 32) {
         // 32-bit cell index: the padded grid has < 2^31 cells
         const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
@@ -473,19 +482,51 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? 4 : 3)
         cv += 32 * dv;
         cw += 32 * dw;
       }
-      if (LERP == ER_LERP_F32) {
-        sx += (double)px;
-        sxx += (double)pxx;
-        syx += (double)pyx;
-      } else {
-        sx += qx;
-        sxx += qxx;
-        syx += qyx;
+      if (LERP == ER_LERP_F32) {  // fp32 row partials (<= nz/32 voxels) -> fp64
+        qx += (double)px;
+        qxx += (double)pxx;
+        qyx += (double)pyx;
+        px = pxx = pyx = 0.f;
       }
-      ty.fold(sy, syy);
     }
+    // fold the group: fixed-order warp reduction in fp64 into the group slot
+    double v[5];
+    v[0] = qx;
+    v[1] = qxx;
+    v[2] = qyx;
+    v[3] = 0.0;
+    v[4] = 0.0;
+    ty.fold(v[3], v[4]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int c = 0; c < 5; ++c) v[c] += __shfl_down_sync(0xffffffffu, v[c], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < 5; ++c) gsum[grp][c] = v[c];
+      grp = atomicAdd(&next_group, 1);
+    }
+    grp = __shfl_sync(0xffffffffu, grp, 0);
   }
-  block_write_partial(sx, sxx, syx, sy, syy, cnt, part);
+  // group-ordered sum (deterministic), integer overlap count
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  __shared__ int cnt_w[kWarps];
+  if (lane == 0) cnt_w[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Partial out{0.0, 0.0, 0.0, 0.0, 0.0, 0};
+    for (int q = 0; q < ngroups; ++q) {
+      out.x += gsum[q][0];
+      out.xx += gsum[q][1];
+      out.yx += gsum[q][2];
+      out.y += gsum[q][3];
+      out.yy += gsum[q][4];
+    }
+    for (int w = 0; w < kWarps; ++w) out.n += cnt_w[w];
+    part[blockIdx.x] = out;
+  }
 }
 
 // Oct re-layout of an 8-bit source (one thread per padded cell).
@@ -653,7 +694,9 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
     return er_set_error(ER_EINVAL, "er_measure_ncc: too many particles for one launch");
   cudaStream_t st = as_stream(stream);
   Partial* part = (Partial*)workspace_dev;
-  const bool use_oct = src->oct_dev && src->dtype == ER_U8 && lerp_mode != ER_LERP_EXACT;
+  // (the oct kernel's per-tile group slots assume a tile of <= kRowsPerTile rows)
+  const bool use_oct = src->oct_dev && src->dtype == ER_U8 && lerp_mode != ER_LERP_EXACT &&
+                       tgt->ny <= kRowsPerTile;
   if (use_oct) {
     const OctGeom og{src->ny + 1, src->nz + 1};
     const unsigned blocks = (unsigned)(P * g.ntiles);
