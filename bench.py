@@ -82,8 +82,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, interval_ms=200):
         self.index = index
+        self.interval_ms = interval_ms
         self.proc = None
         self.lines = []
 
@@ -91,10 +92,15 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # NVML start-up stalls the GPU for tens of ms: let it finish (first
+            # sample read) before the caller starts its timed region
+            t_end = time.time() + 10.0
+            while not self.lines and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -265,32 +271,40 @@ def run_ours(args):
     nvox = t.data.size
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    n_steps = args.warmup + args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(n_steps)]
+    mev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(n_steps)]
+    n_in_sum = []
+
+    def one_step(k):
+        # identical code for warm-up and timed steps (first-use costs such as
+        # lazy kernel loading stay in the warm-up)
+        flush.zero_()  # L2 flush (outside the timed events)
+        ev[k][0].record(stream)
+        run.predict(k)
+        mev[k][0].record(stream)
+        run.measure()
+        mev[k][1].record(stream)
+        n_in_sum.append(run.n_local[: run.plan.count].sum())
+        run.update(k)
+        ev[k][1].record(stream)
+
     for k in range(args.warmup):
-        run.step(k)
+        one_step(k)
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    mev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    n_in_sum = []
-    launches0 = _lib.launch_count
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local, int(os.environ.get("ER_CLOCK_MS", "200"))) as clocks:
         torch.cuda.synchronize(dev)
-        for i in range(args.steps):
-            flush.zero_()  # L2 flush (outside the timed events)
-            k = args.warmup + i
-            ev[i][0].record(stream)
-            run.predict(k)
-            mev[i][0].record(stream)
-            run.measure()
-            mev[i][1].record(stream)
-            n_in_sum.append(run.n_local[: run.plan.count].sum())
-            run.update(k)
-            ev[i][1].record(stream)
+        launches0 = _lib.launch_count
+        for k in range(args.warmup, n_steps):
+            one_step(k)
         torch.cuda.synchronize(dev)
     launches = _lib.launch_count - launches0
+    ev, mev = ev[args.warmup:], mev[args.warmup:]
+    n_in_sum = n_in_sum[args.warmup:]
     step_ms = [a.elapsed_time(b) for a, b in ev]
     meas_ms = [a.elapsed_time(b) for a, b in mev]
     pre_ms = [a[0].elapsed_time(b[0]) for a, b in zip(ev, mev)]
@@ -320,6 +334,7 @@ def run_ours(args):
         "kernel_share_of_step": meas_avg / ms_per_step,
         "pre_ms_per_step": sum(pre_ms) / len(pre_ms),
         "post_ms_per_step": sum(post_ms) / len(post_ms),
+        "post_ms_steps": [round(x, 3) for x in post_ms],
     }
     clk = clocks.summary()
 
