@@ -23,6 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                 "-Xptxas", "-v", "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]
+# extra -D flags for kernel variant experiments (tools/), e.g. "-DER_OCT_PREFETCH=0"
+FLAGS += os.environ.get("ER_NVCC_EXTRA", "").split()
 
 
 def _headers():
@@ -58,6 +60,11 @@ def build(verbose: bool = False) -> str:
     gen_ziggurat.main(os.path.join(CSRC, "zig_tables.h"))
     sources = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
     hdrs = _headers()
+    stamp = os.path.join(OBJDIR, "flags.stamp")
+    if not os.path.exists(stamp) or open(stamp).read() != " ".join(FLAGS):
+        for f in os.listdir(OBJDIR):
+            if f.endswith(".o"):
+                os.remove(os.path.join(OBJDIR, f))
     jobs = []
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(sources), os.cpu_count() or 1))) as ex:
         for f in sources:
@@ -68,6 +75,8 @@ def build(verbose: bool = False) -> str:
         for j in jobs:
             j.result()
     objs = [os.path.join(OBJDIR, f[:-3] + ".o") for f in sources]
+    stamp = os.path.join(OBJDIR, "flags.stamp")
+    open(stamp, "w").write(" ".join(FLAGS))
     if _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static"]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -46,6 +46,19 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerTile = 2048;
 
+#ifndef ER_OCT_PREFETCH
+#define ER_OCT_PREFETCH 0
+#endif
+#ifndef ER_OCT_UNROLL
+#define ER_OCT_UNROLL 1
+#endif
+#define ER_PRAGMA_(x) _Pragma(#x)
+#define ER_UNROLL_(n) ER_PRAGMA_(unroll n)
+#define ER_UNROLL(n) ER_UNROLL_(n)
+#ifndef ER_OCT_MINBLOCKS_F32
+#define ER_OCT_MINBLOCKS_F32 4
+#endif
+
 // kernels_numba.py:88-113, bit-exact (IEEE division, ceil/floor, same guards)
 __device__ __forceinline__ void k_interval(double c0, double slope, double limit, int& klo,
                                            int& khi) {
@@ -350,12 +363,17 @@ struct TgtAcc {
   }
 };
 
+struct RowRec {  // one target row of a 32-row group, in fixed point
+  long long fu0, fv0, fw0;
+  int klo, khi, off, pad;
+};
+
 struct OctGeom {
   int cy, cz;  // padded cell counts along j and k (sy + 1, sz + 1)
 };
 
 template <typename TT, int LERP>
-__global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? 4 : 3)
+__global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOCKS_F32 : 3)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
                        const OctGeom og, Partial* __restrict__ part) {
@@ -386,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? 4 : 3)
   // the result does not depend on which warp ran which group.
   __shared__ double gsum[kRowsPerTile / 32][5];
   __shared__ int next_group;
+  __shared__ RowRec rrec[kWarps][32];
   const int ngroups = (R + 31) / 32;  // <= kRowsPerTile / 32 (make_geom)
   if (threadIdx.x == 0) next_group = kWarps;
   __syncthreads();
@@ -418,25 +437,55 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? 4 : 3)
     // (the +1.0 voxel shift to the padded cell index is an exact integer add,
     // so the cell index below is a plain non-negative 32-bit IMAD chain)
     const long long one = 1LL << (LERP == ER_LERP_F32 ? 32 : 40);
-    const long long fu0 = __double2ll_rn(u0 * F::kScale) + one;
-    const long long fv0 = __double2ll_rn(v0 * F::kScale) + one;
-    const long long fw0 = __double2ll_rn(w0 * F::kScale) + one;
+    // the lane's row record goes to shared memory (broadcast reads below), so
+    // it does not occupy registers across the voxel loop
+    RowRec& mine = rrec[warp][lane];
+    mine.fu0 = __double2ll_rn(u0 * F::kScale) + one;
+    mine.fv0 = __double2ll_rn(v0 * F::kScale) + one;
+    mine.fw0 = __double2ll_rn(w0 * F::kScale) + one;
+    mine.klo = klo;
+    mine.khi = khi;
+    mine.off = off;
     unsigned rows = __ballot_sync(0xffffffffu, khi > klo);
+    __syncwarp();
     while (rows) {
       const int q = __ffs(rows) - 1;
       rows &= rows - 1;
-      const int qlo = __shfl_sync(0xffffffffu, klo, q);
-      const int qhi = __shfl_sync(0xffffffffu, khi, q);
-      const int k0 = qlo + lane;
-      const TT* __restrict__ trow = tgt + __shfl_sync(0xffffffffu, off, q);
-      long long cu = __shfl_sync(0xffffffffu, fu0, q) + (long long)k0 * du;
-      long long cv = __shfl_sync(0xffffffffu, fv0, q) + (long long)k0 * dv;
-      long long cw = __shfl_sync(0xffffffffu, fw0, q) + (long long)k0 * dw;
+      const RowRec& rq = rrec[warp][q];
+      const int qhi = rq.khi;
+      const int k0 = rq.klo + lane;
+      const TT* __restrict__ trow = tgt + rq.off;
+      long long cu = rq.fu0 + (long long)k0 * du;
+      long long cv = rq.fv0 + (long long)k0 * dv;
+      long long cw = rq.fw0 + (long long)k0 * dw;
+      // prefetch distance 1 (fp32 path): the gather of voxel k + 32 is issued
+      // before the arithmetic of voxel k, so two L2 round trips are in flight
+      constexpr bool kPf = (LERP == ER_LERP_F32) && ER_OCT_PREFETCH;
+      uint2 c8n = make_uint2(0u, 0u);
+      TT yn = TT(0);
+      if (kPf && k0 < qhi) {
+        c8n = __ldg(oct + (unsigned)(F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw)));
+        yn = __ldg(trow + k0);
+      }
+      ER_UNROLL(ER_OCT_UNROLL)
       for (int k = k0; k < qhi; k += 32) {
-        // 32-bit cell index: the padded grid has < 2^31 cells
-        const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
-        const uint2 c8 = __ldg(oct + (unsigned)cell);
-        const float yf = ty.add(__ldg(trow + k));
+        uint2 c8;
+        float yf;
+        if (kPf) {
+          c8 = c8n;
+          yf = ty.add(yn);
+          if (k + 32 < qhi) {
+            const long long nu = cu + 32 * du, nv = cv + 32 * dv, nw = cw + 32 * dw;
+            c8n = __ldg(oct + (unsigned)(F::ipart(nu) * cyz + F::ipart(nv) * og.cz +
+                                         F::ipart(nw)));
+            yn = __ldg(trow + k + 32);
+          }
+        } else {
+          // 32-bit cell index: the padded grid has < 2^31 cells
+          const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
+          c8 = __ldg(oct + (unsigned)cell);
+          yf = ty.add(__ldg(trow + k));
+        }
         if (LERP == ER_LERP_F32) {
           const float fu = F::frac32(cu), fv = F::frac32(cv), fw = F::frac32(cw);
           // packed fp32x2 (FFMA2/FADD2): corners paired along k so the u-lerps

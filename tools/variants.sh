@@ -1,0 +1,8 @@
+#!/bin/bash
+# usage: tools/variants.sh "<defines A>" "<defines B>" ...   (run on the GPU box)
+set -e
+for v in "$@"; do
+  ER_NVCC_EXTRA="$v" python paper_2504_19930_b200/_build.py > /dev/null
+  echo "== $v"; python tools/measure_probe.py 2000 f32 3 2>&1 | tail -1
+done
+python paper_2504_19930_b200/_build.py > /dev/null
