@@ -68,6 +68,11 @@ int er_volume_moments(const er_volume *v, double *out_dev, void *stream);
 size_t er_oct_bytes(const er_volume *v);
 int er_build_oct(const er_volume *v, void *oct_dev, void *stream);
 
+/* 256-bin histogram of a u8 volume (exact int64 counts, order-free integer
+ * atomics): the z-score of volume.py:119-130 on 8-bit data is computed from
+ * it (exact integer sums -> numpy-identical mean).  hist_dev: 256 int64. */
+int er_histogram_u8(const er_volume *v, int64_t *hist_dev, void *stream);
+
 /* Classify an f64 device volume: flags_dev[0] = 1 if every voxel is 0 or 1
  * (volume.py:138-140), flags_dev[1] = 1 if every voxel is exactly
  * representable in fp32.  Used to pick a lossless storage type. */

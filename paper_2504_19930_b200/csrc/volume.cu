@@ -90,6 +90,36 @@ __global__ void convert_kernel(const double* __restrict__ v, long long n, D* __r
     out[q] = (D)v[q];
 }
 
+__global__ void histogram_u8_kernel(const uint8_t* __restrict__ v, long long n,
+                                    unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int h[256];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  // 16 bytes per thread per step (vectorised read), integer shared atomics
+  const long long n16 = n / 16;
+  const uint4* v16 = reinterpret_cast<const uint4*>(v);
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n16;
+       q += (long long)gridDim.x * blockDim.x) {
+    const uint4 w = __ldg(v16 + q);
+    const unsigned words[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) atomicAdd(&h[(words[i] >> (8 * b)) & 0xffu], 1u);
+    }
+  }
+  for (long long q = n16 * 16 + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x)
+    atomicAdd(&h[v[q]], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x)
+    if (h[b]) atomicAdd(hist + b, (unsigned long long)h[b]);
+}
+
+__global__ void zero_u64_kernel(unsigned long long* p, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
+}
+
 template <typename T>
 void launch_moments(const void* data, long long n, double* part, cudaStream_t st) {
   moments_partial_kernel<T><<<kMomBlocks, kMomThreads, 0, st>>>((const T*)data, n, part);
@@ -142,6 +172,24 @@ extern "C" int er_convert_f64(const double* data_dev, int64_t n, int32_t dst_dty
     case ER_F32: convert_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(data_dev, n, (float*)dst_dev); break;
     default: return er_set_error(ER_EINVAL, "er_convert_f64: dst must be u8 or f32");
   }
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_histogram_u8(const er_volume* v, int64_t* hist_dev, void* stream) {
+  if (!v || !v->data_dev || !hist_dev || v->dtype != ER_U8)
+    return er_set_error(ER_EINVAL, "er_histogram_u8: needs a u8 volume and a 256-bin buffer");
+  const long long n = (long long)v->nx * v->ny * v->nz;
+  cudaStream_t st = as_stream(stream);
+  zero_u64_kernel<<<1, 256, 0, st>>>((unsigned long long*)hist_dev, 256);
+  // the data pointer of a torch uint8 tensor is at least 256-byte aligned
+  if ((reinterpret_cast<uintptr_t>(v->data_dev) & 15) != 0)
+    return er_set_error(ER_EINVAL, "er_histogram_u8: data must be 16-byte aligned");
+  long long blocks = (n / 16 + 255) / 256;
+  if (blocks > ER_NUM_SMS_B200 * 4) blocks = ER_NUM_SMS_B200 * 4;
+  if (blocks < 1) blocks = 1;
+  histogram_u8_kernel<<<(unsigned)blocks, 256, 0, st>>>((const uint8_t*)v->data_dev, n,
+                                                         (unsigned long long*)hist_dev);
   ER_CHECK_LAUNCH();
   return ER_OK;
 }

@@ -73,6 +73,7 @@ class DeviceVolume:
     origin: tuple
     moments: object          # torch f64 [ER_MOMENTS_DOUBLES], [0]=sum, [1]=sumsq of stored
     dtype_code: int
+    shared: object = None    # _SharedU8 for 8-bit storage (oct / histogram cache)
 
     @property
     def desc_ptr(self):
@@ -83,16 +84,53 @@ class DeviceVolume:
         return int(self.storage.numel() * self.storage.element_size())
 
     def ensure_oct(self):
-        """Build (once) the oct re-layout of a u8 volume used as a measurement
-        source: all 8 trilinear corners of a cell in one 8-byte word."""
+        """Build (once per 8-bit array) the oct re-layout used by the
+        measurement fast path: all 8 trilinear corners of a cell in 8 bytes."""
         if self.dtype_code != _lib.ER_U8 or self.desc.oct_dev:
             return
+        sh = self.shared
+        if sh is None or sh.oct is None:
+            t = torch()
+            nbytes = int(_lib.load().er_oct_bytes(ctypes.byref(self.desc)))
+            oct_ = t.empty(nbytes, dtype=t.uint8, device=self.storage.device)
+            _lib.call("er_build_oct", ctypes.byref(self.desc), ptr(oct_),
+                      stream_ptr(self.storage.device))
+            if sh is None:
+                self.oct = oct_
+            else:
+                sh.oct = oct_
+        self.desc.oct_dev = (sh.oct if sh is not None else self.oct).data_ptr()
+
+    def histogram(self) -> np.ndarray:
+        """Exact 256-bin histogram of 8-bit storage (er_histogram_u8), cached."""
+        if self.dtype_code != _lib.ER_U8:
+            raise ValueError("histogram needs 8-bit storage")
+        sh = self.shared
+        if sh is not None and sh.hist is not None:
+            return sh.hist
         t = torch()
-        nbytes = int(_lib.load().er_oct_bytes(ctypes.byref(self.desc)))
-        self.oct = t.empty(nbytes, dtype=t.uint8, device=self.storage.device)
-        _lib.call("er_build_oct", ctypes.byref(self.desc), ptr(self.oct),
+        h = t.empty(256, dtype=t.int64, device=self.storage.device)
+        _lib.call("er_histogram_u8", ctypes.byref(self.desc), ptr(h),
                   stream_ptr(self.storage.device))
-        self.desc.oct_dev = self.oct.data_ptr()
+        hist = h.cpu().numpy()
+        if sh is not None:
+            sh.hist = hist
+        return hist
+
+
+@dataclass
+class _SharedU8:
+    """One device upload of one raw 8-bit host array, shared by every volume
+    (any affine) built on it: storage, stored-value moments, oct, histogram."""
+
+    raw_ref: object
+    storage: object
+    moments: object
+    oct: object = None
+    hist: object = None
+
+
+_U8_STORE: dict = {}
 
 
 def _make_desc(storage, code, dims, alpha, gamma):
@@ -105,8 +143,33 @@ def _make_desc(storage, code, dims, alpha, gamma):
     return d
 
 
-def upload_array(data: np.ndarray, device, *, codec=None, pinned_staging=False):
-    """Upload one fp64 (or raw uint8 codec) volume and pick its storage type."""
+def _shared_u8(raw: np.ndarray, device, pinned_staging=False) -> _SharedU8:
+    import weakref
+
+    key = (id(raw), device.index)
+    hit = _U8_STORE.get(key)
+    if hit is not None and hit.raw_ref() is raw:
+        return hit
+    t = torch()
+    flat = np.ascontiguousarray(raw, dtype=np.uint8).reshape(-1)
+    host = t.from_numpy(flat)
+    if pinned_staging and not host.is_pinned():
+        host = host.pin_memory()
+    storage = host.to(device, non_blocking=host.is_pinned())
+    desc = _make_desc(storage, _lib.ER_U8, raw.shape, 1.0, 0.0)
+    moments = t.empty(_lib.ER_MOMENTS_DOUBLES, dtype=t.float64, device=device)
+    _lib.call("er_volume_moments", ctypes.byref(desc), ptr(moments), stream_ptr(device))
+    try:
+        ref = weakref.ref(raw, lambda _r, k=key: _U8_STORE.pop(k, None))
+    except TypeError:  # pragma: no cover - non-weakrefable array
+        ref = (lambda r=raw: r)
+    sh = _SharedU8(ref, storage, moments)
+    _U8_STORE[key] = sh
+    return sh
+
+
+def upload_array(data: np.ndarray, device, *, pinned_staging=False):
+    """Upload one fp64 volume and pick a lossless storage type on the device."""
     t = torch()
     dims = tuple(int(x) for x in data.shape)
     if len(dims) != 3:
@@ -114,41 +177,34 @@ def upload_array(data: np.ndarray, device, *, codec=None, pinned_staging=False):
     if int(np.prod(dims)) >= 2**31:
         raise ValueError("volume too large for one device descriptor (>= 2^31 voxels)")
     stream = stream_ptr(device)
-    if codec is not None:
-        raw = np.ascontiguousarray(codec.raw, dtype=np.uint8).reshape(-1)
-        host = t.from_numpy(raw)
-        if pinned_staging:
-            host = host.pin_memory()
-        storage = host.to(device, non_blocking=pinned_staging)
-        code, alpha, gamma = _lib.ER_U8, 1.0 / codec.std, -codec.mean / codec.std
+    flat = np.ascontiguousarray(data, dtype=np.float64).reshape(-1)
+    host = t.from_numpy(flat)
+    if pinned_staging:
+        host = host.pin_memory()
+    f64 = host.to(device, non_blocking=pinned_staging)
+    flags = t.empty(3, dtype=t.int32, device=device)
+    _lib.call("er_classify_f64", ptr(f64), f64.numel(), ptr(flags), stream)
+    binary, f32ok, u8ok = (bool(x) for x in flags.tolist())
+    if binary or u8ok:
+        storage = t.empty(f64.numel(), dtype=t.uint8, device=device)
+        _lib.call("er_convert_f64", ptr(f64), f64.numel(), _lib.ER_U8, ptr(storage), stream)
+        code = _lib.ER_U8
+    elif f32ok:
+        storage = t.empty(f64.numel(), dtype=t.float32, device=device)
+        _lib.call("er_convert_f64", ptr(f64), f64.numel(), _lib.ER_F32, ptr(storage), stream)
+        code = _lib.ER_F32
     else:
-        flat = np.ascontiguousarray(data, dtype=np.float64).reshape(-1)
-        host = t.from_numpy(flat)
-        if pinned_staging:
-            host = host.pin_memory()
-        f64 = host.to(device, non_blocking=pinned_staging)
-        flags = t.empty(3, dtype=t.int32, device=device)
-        _lib.call("er_classify_f64", ptr(f64), f64.numel(), ptr(flags), stream)
-        binary, f32ok, u8ok = (bool(x) for x in flags.tolist())
-        alpha, gamma = 1.0, 0.0
-        if binary or u8ok:
-            storage = t.empty(f64.numel(), dtype=t.uint8, device=device)
-            _lib.call("er_convert_f64", ptr(f64), f64.numel(), _lib.ER_U8, ptr(storage), stream)
-            code = _lib.ER_U8
-        elif f32ok:
-            storage = t.empty(f64.numel(), dtype=t.float32, device=device)
-            _lib.call("er_convert_f64", ptr(f64), f64.numel(), _lib.ER_F32, ptr(storage), stream)
-            code = _lib.ER_F32
-        else:
-            storage, code = f64, _lib.ER_F64
-    desc = _make_desc(storage, code, dims, alpha, gamma)
+        storage, code = f64, _lib.ER_F64
+    desc = _make_desc(storage, code, dims, 1.0, 0.0)
     moments = t.empty(_lib.ER_MOMENTS_DOUBLES, dtype=t.float64, device=device)
     _lib.call("er_volume_moments", ctypes.byref(desc), ptr(moments), stream)
     return storage, desc, moments, code
 
 
 def device_volume(v, device=None) -> DeviceVolume:
-    """Device copy of a Volume3 (cached on the object; volumes are immutable)."""
+    """Device copy of a Volume3 (cached on the object; volumes are immutable).
+    8-bit codec volumes share one upload per raw array; their fp64 ``data``
+    is never touched."""
     dev = require_cuda(device)
     cache = getattr(v, "_er_device_cache", None)
     if cache is None:
@@ -158,9 +214,17 @@ def device_volume(v, device=None) -> DeviceVolume:
     hit = cache.get(key)
     if hit is not None:
         return hit
-    storage, desc, moments, code = upload_array(v.data, dev, codec=getattr(v, "codec", None))
-    dv = DeviceVolume(storage, desc, tuple(v.dims), tuple(v.spacing), tuple(v.origin), moments,
-                      code)
+    codec = getattr(v, "codec", None)
+    if codec is not None:
+        sh = _shared_u8(codec.raw, dev)
+        desc = _make_desc(sh.storage, _lib.ER_U8, v.dims, 1.0 / codec.std,
+                          -codec.mean / codec.std)
+        dv = DeviceVolume(sh.storage, desc, tuple(v.dims), tuple(v.spacing), tuple(v.origin),
+                          sh.moments, _lib.ER_U8, sh)
+    else:
+        storage, desc, moments, code = upload_array(v.data, dev)
+        dv = DeviceVolume(storage, desc, tuple(v.dims), tuple(v.spacing), tuple(v.origin),
+                          moments, code)
     cache[key] = dv
     return dv
 
@@ -192,3 +256,18 @@ class Workspace:
 
 
 WORKSPACE = Workspace()
+
+
+def u8_histogram(raw: np.ndarray, device=None) -> np.ndarray:
+    """Exact 256-bin histogram of a raw 8-bit host array, computed on the
+    device from the (shared, cached) upload -- the ingest step of the z-score
+    on 8-bit echo data (volume.normalize_zscore)."""
+    dev = require_cuda(device)
+    sh = _shared_u8(raw, dev)
+    if sh.hist is None:
+        t = torch()
+        desc = _make_desc(sh.storage, _lib.ER_U8, raw.shape, 1.0, 0.0)
+        h = t.empty(256, dtype=t.int64, device=dev)
+        _lib.call("er_histogram_u8", ctypes.byref(desc), ptr(h), stream_ptr(dev))
+        sh.hist = h.cpu().numpy()
+    return sh.hist

@@ -1,0 +1,170 @@
+"""Timings of the BASELINE.json configs beyond the bench's headline (C2).
+
+    python tools/bench_configs.py [c1] [c3] [c4] [c5] [--cpu]
+
+C1  mask SMC, 64^3 phantom pair, 500 particles x 20 iterations (the SPEC
+    acceptance case); GPU register_smc e2e vs the CPU reference algorithm
+    (oracle/smc.py + the bit-exact C kernel) on all host threads, same seed.
+C3  register_sequence, mask mode, 30-frame 176x176x208 echo cycle,
+    2000 particles x 50 iterations, then warp + score of all 30 frames.
+C4  exhaustive search, default GridSpec (9^6 = 531,441 nodes), C2 pair.
+C5  particle sweep 1k..256k on a 256^3 z-scored u8 pair: one measurement
+    launch per P (evals/s, sampled/s, roofline fraction).
+Writes one JSON object per config to stdout (and profiles/ via tee).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+
+def sync():
+    torch.cuda.synchronize()
+
+
+def truth_err(est, truth):
+    d = est.to_array() - truth.to_array()
+    return {"rot_err_deg": [round(math.degrees(x), 4) for x in d[:3]],
+            "trans_err_mm": [round(float(x), 4) for x in d[3:]]}
+
+
+def c1(cpu=False):
+    from paper_2504_19930_b200 import (Executor, PhantomSpec, RigidParams, SmcConfig,
+                                       make_pair, make_phantom, register_smc)
+
+    seq, masks = make_phantom(PhantomSpec(dims=(64, 64, 64), frames=1, seed=0))
+    truth = RigidParams(math.radians(5), math.radians(-8), math.radians(4), 6.0, -4.0, 3.0)
+    case = make_pair(seq, masks, truth)
+    tm, sm = case.target_masks[0], case.source_masks[0]
+    cfg = SmcConfig(mode="mask", n_particles=500, n_iterations=20, seed=0)
+    register_smc(tm, sm, cfg, Executor())  # warm-up
+    times = []
+    for _ in range(5):
+        import copy
+
+        a, b = copy.copy(tm), copy.copy(sm)
+        for v in (a, b):
+            if hasattr(v, "_er_device_cache"):
+                object.__delattr__(v, "_er_device_cache")
+        sync()
+        t0 = time.perf_counter()
+        est, tr = register_smc(a, b, cfg, Executor())
+        sync()
+        times.append(time.perf_counter() - t0)
+    out = {"config": "C1 mask SMC 64^3, 500 x 20", "gpu_registration_ms": 1e3 * min(times),
+           "gpu_registration_ms_median": 1e3 * sorted(times)[2],
+           "evals_per_s": 500 * 64 ** 3 * 20 / min(times), **truth_err(est, truth)}
+    if cpu:
+        from oracle import kernels as ok
+        from oracle import smc as osmc
+
+        ok.build()
+        geom = (tm.dims, tm.spacing, tm.origin)
+        t0 = time.perf_counter()
+        oest, _ = osmc.register(tm.data, sm.data, geom, geom,
+                                osmc.Cfg(mode="mask", n_particles=500, n_iterations=20, seed=0))
+        cpu_s = time.perf_counter() - t0
+        d = est.to_array() - oest
+        out.update({"cpu_reference_registration_s": cpu_s, "cpu_threads": ok.max_threads(),
+                    "speedup_vs_cpu": cpu_s / min(times),
+                    "gpu_vs_cpu_estimate_max_abs_diff": float(np.abs(d).max())})
+    return out
+
+
+def c3():
+    from paper_2504_19930_b200 import Executor, SmcConfig, register_sequence
+    from paper_2504_19930_b200.phantom import echo_case
+
+    t0 = time.perf_counter()
+    case = echo_case(frames=30, seed=0)
+    gen_s = time.perf_counter() - t0
+    cfg = SmcConfig(mode="mask", n_particles=2000, n_iterations=50, seed=0)
+    # warm-up on a 2-frame slice
+    from paper_2504_19930_b200 import Sequence4
+
+    register_sequence(Sequence4(case.target.frames[:2]), Sequence4(case.source.frames[:2]),
+                      case.target_masks[:2], case.source_masks[:2],
+                      SmcConfig(mode="mask", n_particles=64, n_iterations=2), Executor())
+    sync()
+    t0 = time.perf_counter()
+    rep = register_sequence(case.target, case.source, case.target_masks, case.source_masks,
+                            cfg, Executor())
+    sync()
+    wall = time.perf_counter() - t0
+    return {"config": "C3 mask SMC + 30-frame 4D warp/score, 176x176x208, 2000 x 50",
+            "register_sequence_s": wall, "phantom_generation_s": gen_s,
+            "dsc_before_mean": rep.aggregates["dsc_before_mean"],
+            "dsc_after_mean": rep.aggregates["dsc_after_mean"],
+            "ncc_after_mean": rep.aggregates["ncc_after_mean"],
+            "estimate_deg_mm": rep.estimate_deg_mm}
+
+
+def c4():
+    import bench
+    from paper_2504_19930_b200 import Executor, GridSpec, register_exhaustive
+
+    t, s, case = bench.make_workload()
+    g = GridSpec()
+    small = GridSpec(half_counts=(1, 1, 1, 1, 1, 1))
+    register_exhaustive(t, s, small, Executor())
+    sync()
+    t0 = time.perf_counter()
+    best, val = register_exhaustive(t, s, g, Executor())
+    sync()
+    wall = time.perf_counter() - t0
+    return {"config": "C4 exhaustive 9^6 grid, C2 pair", "nodes": g.n_nodes,
+            "seconds": wall, "evals_per_s": g.n_nodes * t.data.size / wall,
+            "best_deg_mm": [math.degrees(x) for x in best.to_array()[:3]]
+            + list(best.to_array()[3:]), "best_ncc": float(val)}
+
+
+def c5(pmax=262144):
+    from paper_2504_19930_b200 import SmcConfig, Volume3, normalize_zscore, ops
+    from paper_2504_19930_b200 import smc as dsmc
+    from paper_2504_19930_b200.backend import Executor
+    from paper_2504_19930_b200.phantom import echo_case
+
+    case = echo_case(dims=(256, 256, 256), spacing=(0.8, 0.8, 0.8), frames=1, seed=0)
+    t = normalize_zscore(case.target.frames[0])
+    s = normalize_zscore(case.source.frames[0])
+    rows = []
+    p = 1024
+    while p <= pmax:
+        cfg = SmcConfig(mode="image", n_particles=p, n_iterations=1, seed=0)
+        run = dsmc.DeviceSmcRun(t, s, cfg, Executor())
+        run.predict(0)
+        run.measure()
+        sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run.measure()
+        e1.record()
+        sync()
+        ms = e0.elapsed_time(e1)
+        nin = float(run.n_local[:p].sum().item())
+        rows.append({"particles": p, "ms": ms, "evals_per_s": p * t.data.size / (ms * 1e-3),
+                     "sampled_per_s": nin / (ms * 1e-3),
+                     "hbm_frac_9B": nin * 9 / (ms * 1e-3) / 6535.4e9})
+        print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
+        del run
+        torch.cuda.empty_cache()
+        p *= 4
+    return {"config": "C5 particle sweep on 256^3, 1 GPU", "rows": rows}
+
+
+if __name__ == "__main__":
+    which = [a for a in sys.argv[1:] if not a.startswith("--")] or ["c1", "c3", "c4", "c5"]
+    for w in which:
+        fn = globals()[w]
+        res = fn(cpu=("--cpu" in sys.argv)) if w == "c1" else fn()
+        print(json.dumps(res), flush=True)
