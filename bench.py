@@ -253,13 +253,13 @@ def run_ours(args):
             print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    launched = "WORLD_SIZE" in os.environ  # torchrun: NCCL group even at N = 1
+    if launched:
         import torch.distributed as td
 
         td.init_process_group("nccl", device_id=dev)
-    from paper_2504_19930_b200 import Executor, SmcConfig, _lib, register_smc
+    from paper_2504_19930_b200 import Executor, SmcConfig, _lib
     from paper_2504_19930_b200 import smc as dsmc
-    from paper_2504_19930_b200.backend import Executor as _E  # noqa: F401
 
     precision = args.precision or Executor().precision
     ex = Executor(precision=precision, device=local)
@@ -367,7 +367,7 @@ def run_ours(args):
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if launched:
         torch.distributed.destroy_process_group()
 
 

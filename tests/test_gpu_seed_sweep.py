@@ -73,3 +73,32 @@ def test_image_mode_seed_sweep(precision):
     deg, vox = _sweep(tv, sv, "image", 96, 10, precision, t_limit=6.0, r_limit=8.0)
     print(f"img {precision}: worst |d rot| {deg:.3g} deg, |d trans| {vox:.3g} vox")
     assert deg <= 0.1 and vox <= 0.1
+
+
+@pytest.fixture(scope="module")
+def echo_pair():
+    from paper_2504_19930_b200 import normalize_zscore
+    from paper_2504_19930_b200.phantom import echo_case
+
+    case = echo_case(frames=1, seed=3)
+    return normalize_zscore(case.target.frames[0]), normalize_zscore(case.source.frames[0])
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_c2_shaped_echo_free_run_matches_reference_algorithm(echo_pair, seed):
+    """BASELINE C2 shape (176x176x208 u8 echo pair, z-scored, 8-bit codec +
+    oct fast path, fp32 lerps) -- a shortened run (256 particles x 8
+    iterations) so the CPU reference algorithm finishes in seconds."""
+    from paper_2504_19930_b200 import Executor, SmcConfig, register_smc
+
+    tv, sv = echo_pair
+    cfg = SmcConfig(mode="image", n_particles=256, n_iterations=8, seed=seed)
+    est, tr = register_smc(tv, sv, cfg, Executor(precision="f32"))
+    geom = (tv.dims, tv.spacing, tv.origin)
+    oest, otr = osmc.register(tv.data, sv.data, geom, geom,
+                              osmc.Cfg(mode="image", n_particles=256, n_iterations=8, seed=seed))
+    d = est.to_array() - oest
+    assert np.all(np.degrees(np.abs(d[:3])) <= 0.1), d
+    assert np.all(np.abs(d[3:]) / np.asarray(tv.spacing) <= 0.1), d
+    assert tr.resampled == otr.resampled
+    np.testing.assert_allclose(tr.max_measurement, otr.max_measurement, rtol=1e-4)
