@@ -52,6 +52,26 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_OCT_UNROLL
 #define ER_OCT_UNROLL 1
 #endif
+// cache policy of the oct gathers: 0 = ld.global.nc (L1 allocate), 1 = .cg
+// (L2 only), 2 = .cs (streaming)
+#ifndef ER_OCT_LDPOLICY
+#define ER_OCT_LDPOLICY 0
+#endif
+#ifndef ER_FRAC_I2F
+#define ER_FRAC_I2F 1
+#endif
+#ifndef ER_OCT_TILE_MAJOR
+#define ER_OCT_TILE_MAJOR 1
+#endif
+__device__ __forceinline__ uint2 ld_oct(const uint2* p) {
+#if ER_OCT_LDPOLICY == 1
+  return __ldcg(p);
+#elif ER_OCT_LDPOLICY == 2
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
 #define ER_PRAGMA_(x) _Pragma(#x)
 #define ER_UNROLL_(n) ER_PRAGMA_(unroll n)
 #define ER_UNROLL(n) ER_UNROLL_(n)
@@ -319,6 +339,9 @@ struct Fix {
   static constexpr double kScale = (double)(1ULL << FB);
   __device__ __forceinline__ static int ipart(long long q) { return (int)(q >> FB); }
   __device__ __forceinline__ static float frac32(long long q) {
+#if ER_FRAC_I2F
+    if (FB == 32) return __uint2float_rz((unsigned)q) * 2.3283064365386963e-10f;  // 2^-32
+#endif
     // top 23 fraction bits -> [1, 2) - 1
     const unsigned m = (unsigned)((unsigned long long)q >> (FB - 23)) & 0x7FFFFFu;
     return __int_as_float(0x3F800000u | m) - 1.0f;
@@ -370,6 +393,7 @@ struct RowRec {  // one target row of a 32-row group, in fixed point
 
 struct OctGeom {
   int cy, cz;  // padded cell counts along j and k (sy + 1, sz + 1)
+  long long P; // particles in the launch (tile-major block order)
 };
 
 template <typename TT, int LERP>
@@ -378,8 +402,18 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOC
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
                        const OctGeom og, Partial* __restrict__ part) {
   using F = Fix<LERP == ER_LERP_F32 ? 32 : 40>;
+#if ER_OCT_TILE_MAJOR
+  // tile-major launch order: the CTAs resident at any moment work on the same
+  // target slab for many particles, so the union of their source footprints
+  // (and the shared target slab) stays L2-resident even when the oct volume
+  // does not fit (256^3: 136 MB)
+  const int tile = (int)(blockIdx.x / og.P);
+  const long long p = blockIdx.x - (long long)tile * og.P;
+#else
   const int tile = blockIdx.x % g.ntiles;
   const long long p = blockIdx.x / g.ntiles;
+#endif
+  const long long slot = p * g.ntiles + tile;
   // the particle's affine lives in shared memory: it is only needed once per
   // 32-row group, and keeping 12 doubles out of the registers of the inner
   // loop is what lets this kernel run 3 CTAs/SM without spills
@@ -483,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOC
         } else {
           // 32-bit cell index: the padded grid has < 2^31 cells
           const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
-          c8 = __ldg(oct + (unsigned)cell);
+          c8 = ld_oct(oct + (unsigned)cell);
           yf = ty.add(__ldg(trow + k));
         }
         if (LERP == ER_LERP_F32) {
@@ -574,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOC
       out.yy += gsum[q][4];
     }
     for (int w = 0; w < kWarps; ++w) out.n += cnt_w[w];
-    part[blockIdx.x] = out;
+    part[slot] = out;
   }
 }
 
@@ -747,7 +781,7 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
   const bool use_oct = src->oct_dev && src->dtype == ER_U8 && lerp_mode != ER_LERP_EXACT &&
                        tgt->ny <= kRowsPerTile;
   if (use_oct) {
-    const OctGeom og{src->ny + 1, src->nz + 1};
+    const OctGeom og{src->ny + 1, src->nz + 1, (long long)P};
     const unsigned blocks = (unsigned)(P * g.ntiles);
     const uint2* oct = (const uint2*)src->oct_dev;
 #define ER_OCT(TT, L) \
