@@ -46,8 +46,8 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerTile = 2048;
 
-#ifndef ER_OCT_PREFETCH
-#define ER_OCT_PREFETCH 0
+#ifndef ER_OCT_HALF
+#define ER_OCT_HALF 1
 #endif
 #ifndef ER_OCT_UNROLL
 #define ER_OCT_UNROLL 1
@@ -482,44 +482,37 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOC
     mine.off = off;
     unsigned rows = __ballot_sync(0xffffffffu, khi > klo);
     __syncwarp();
+    // kLanes lanes per row: 32 (one row at a time) or 16 (two rows side by
+    // side on the half-warps: for nz = 208 = 13 x 16 no lane idles at the row
+    // end, and each lane's per-row overhead is paid over twice the voxels)
+    constexpr int kLanes = ER_OCT_HALF ? 16 : 32;
+    const int sub = lane & (kLanes - 1);
     while (rows) {
-      const int q = __ffs(rows) - 1;
+      int q = __ffs(rows) - 1;
       rows &= rows - 1;
-      const RowRec& rq = rrec[warp][q];
-      const int qhi = rq.khi;
-      const int k0 = rq.klo + lane;
-      const TT* __restrict__ trow = tgt + rq.off;
-      long long cu = rq.fu0 + (long long)k0 * du;
-      long long cv = rq.fv0 + (long long)k0 * dv;
-      long long cw = rq.fw0 + (long long)k0 * dw;
-      // prefetch distance 1 (fp32 path): the gather of voxel k + 32 is issued
-      // before the arithmetic of voxel k, so two L2 round trips are in flight
-      constexpr bool kPf = (LERP == ER_LERP_F32) && ER_OCT_PREFETCH;
-      uint2 c8n = make_uint2(0u, 0u);
-      TT yn = TT(0);
-      if (kPf && k0 < qhi) {
-        c8n = __ldg(oct + (unsigned)(F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw)));
-        yn = __ldg(trow + k0);
+      if (kLanes == 16) {
+        const int q2 = rows ? __ffs(rows) - 1 : -1;
+        if (q2 >= 0) rows &= rows - 1;
+        if (lane >= 16) q = q2;
+      }
+      int qhi = 0, k0 = 1;
+      const TT* __restrict__ trow = tgt;
+      long long cu = 0, cv = 0, cw = 0;
+      if (q >= 0) {
+        const RowRec& rq = rrec[warp][q];
+        qhi = rq.khi;
+        k0 = rq.klo + sub;
+        trow = tgt + rq.off;
+        cu = rq.fu0 + (long long)k0 * du;
+        cv = rq.fv0 + (long long)k0 * dv;
+        cw = rq.fw0 + (long long)k0 * dw;
       }
       ER_UNROLL(ER_OCT_UNROLL)
-      for (int k = k0; k < qhi; k += 32) {
-        uint2 c8;
-        float yf;
-        if (kPf) {
-          c8 = c8n;
-          yf = ty.add(yn);
-          if (k + 32 < qhi) {
-            const long long nu = cu + 32 * du, nv = cv + 32 * dv, nw = cw + 32 * dw;
-            c8n = __ldg(oct + (unsigned)(F::ipart(nu) * cyz + F::ipart(nv) * og.cz +
-                                         F::ipart(nw)));
-            yn = __ldg(trow + k + 32);
-          }
-        } else {
-          // 32-bit cell index: the padded grid has < 2^31 cells
-          const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
-          c8 = ld_oct(oct + (unsigned)cell);
-          yf = ty.add(__ldg(trow + k));
-        }
+      for (int k = k0; k < qhi; k += kLanes) {
+        // 32-bit cell index: the padded grid has < 2^31 cells
+        const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
+        const uint2 c8 = ld_oct(oct + (unsigned)cell);
+        const float yf = ty.add(__ldg(trow + k));
         if (LERP == ER_LERP_F32) {
           const float fu = F::frac32(cu), fv = F::frac32(cv), fw = F::frac32(cw);
           // packed fp32x2 (FFMA2/FADD2): corners paired along k so the u-lerps
@@ -561,11 +554,11 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOC
           qxx = fma(x, x, qxx);
           qyx = fma((double)yf, x, qyx);
         }
-        cu += 32 * du;
-        cv += 32 * dv;
-        cw += 32 * dw;
+        cu += kLanes * du;
+        cv += kLanes * dv;
+        cw += kLanes * dw;
       }
-      if (LERP == ER_LERP_F32) {  // fp32 row partials (<= nz/32 voxels) -> fp64
+      if (LERP == ER_LERP_F32) {  // fp32 row partials (<= nz/kLanes voxels) -> fp64
         qx += (double)px;
         qxx += (double)pxx;
         qyx += (double)pyx;
