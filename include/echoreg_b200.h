@@ -46,6 +46,7 @@ typedef struct er_volume {
   int32_t nx, ny, nz;
   double alpha, gamma;  /* value = alpha * stored + gamma */
   const void *oct_dev;  /* optional er_build_oct() re-layout of a u8 volume, or NULL */
+  const void *bitoct_dev; /* optional er_build_bitoct() re-layout of a binary volume */
 } er_volume;
 
 int er_abi_version(void);
@@ -67,6 +68,13 @@ int er_volume_moments(const er_volume *v, double *out_dev, void *stream);
  * (used for lerp modes F32/F64; LERP_EXACT always gathers the plain copy). */
 size_t er_oct_bytes(const er_volume *v);
 int er_build_oct(const er_volume *v, void *oct_dev, void *stream);
+
+/* Bit-oct re-layout of a BINARY u8 volume (values 0/1): the same padded
+ * cells with the 8 corners as the 8 bits of one byte (bit b = byte b of the
+ * oct word).  (nx+1)(ny+1)(nz+1) bytes.  Set er_volume.bitoct_dev to enable
+ * the mask fast path (1-byte gathers; uniform cells skip the lerps). */
+size_t er_bitoct_bytes(const er_volume *v);
+int er_build_bitoct(const er_volume *v, void *bitoct_dev, void *stream);
 
 /* 256-bin histogram of a u8 volume (exact int64 counts, order-free integer
  * atomics): the z-score of volume.py:119-130 on 8-bit data is computed from

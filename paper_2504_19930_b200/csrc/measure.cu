@@ -43,6 +43,11 @@ struct Geom {
 };
 
 constexpr int kThreads = 256;
+#ifndef ER_OCT_THREADS
+#define ER_OCT_THREADS 256
+#endif
+constexpr int kOctThreads = ER_OCT_THREADS;  // oct fast path CTA size
+constexpr int kOctWarps = kOctThreads / 32;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerTile = 2048;
 
@@ -396,8 +401,10 @@ struct OctGeom {
   long long P; // particles in the launch (tile-major block order)
 };
 
-template <typename TT, int LERP>
-__global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOCKS_F32 : 3)
+// BITS = 1: `oct` points at the bit-oct layout of a binary source (1 byte per
+// cell) and the lerps run in fp32 (row partials folded per row as below).
+template <typename TT, int LERP, int BITS = 0>
+__global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOCKS_F32 : 3)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
                        const OctGeom og, Partial* __restrict__ part) {
@@ -438,9 +445,9 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOC
   // the result does not depend on which warp ran which group.
   __shared__ double gsum[kRowsPerTile / 32][5];
   __shared__ int next_group;
-  __shared__ RowRec rrec[kWarps][32];
+  __shared__ RowRec rrec[kOctWarps][32];
   const int ngroups = (R + 31) / 32;  // <= kRowsPerTile / 32 (make_geom)
-  if (threadIdx.x == 0) next_group = kWarps;
+  if (threadIdx.x == 0) next_group = kOctWarps;
   __syncthreads();
   int cnt = 0;
 
@@ -511,6 +518,33 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOC
       for (int k = k0; k < qhi; k += kLanes) {
         // 32-bit cell index: the padded grid has < 2^31 cells
         const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
+        if (BITS) {
+          // binary source: one byte = the cell's 8 corner bits; uniform cells
+          // (all 0 / all 1) are exact without interpolation
+          const unsigned c = __ldg(reinterpret_cast<const uint8_t*>(oct) + (unsigned)cell);
+          const float yf = ty.add(__ldg(trow + k));
+          float x = (c == 0xFFu) ? 1.0f : 0.0f;
+          if (c != 0u && c != 0xFFu) {
+            const float fu = F::frac32(cu), fv = F::frac32(cv), fw = F::frac32(cw);
+            auto bit = [c](int b) { return ((c >> b) & 1u) ? 1.0f : 0.0f; };
+            const float2 P0 = make_float2(bit(0), bit(4)), P1 = make_float2(bit(1), bit(5));
+            const float2 Q0 = make_float2(bit(2), bit(6)), Q1 = make_float2(bit(3), bit(7));
+            const float2 fu2 = make_float2(fu, fu), fv2 = make_float2(fv, fv);
+            const float2 cP = __ffma2_rn(fu2, __fadd2_rn(P1, make_float2(-P0.x, -P0.y)), P0);
+            const float2 cQ = __ffma2_rn(fu2, __fadd2_rn(Q1, make_float2(-Q0.x, -Q0.y)), Q0);
+            const float2 cc = __ffma2_rn(fv2, __fadd2_rn(cQ, make_float2(-cP.x, -cP.y)), cP);
+            x = fmaf(fw, cc.y - cc.x, cc.x);
+          }
+          const float2 acc = __ffma2_rn(make_float2(x, x), make_float2(1.0f, x),
+                                        make_float2(px, pxx));
+          px = acc.x;
+          pxx = acc.y;
+          pyx = fmaf(yf, x, pyx);
+          cu += kLanes * du;
+          cv += kLanes * dv;
+          cw += kLanes * dw;
+          continue;
+        }
         const uint2 c8 = ld_oct(oct + (unsigned)cell);
         const float yf = ty.add(__ldg(trow + k));
         if (LERP == ER_LERP_F32) {
@@ -558,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOC
         cv += kLanes * dv;
         cw += kLanes * dw;
       }
-      if (LERP == ER_LERP_F32) {  // fp32 row partials (<= nz/kLanes voxels) -> fp64
+      if (LERP == ER_LERP_F32 || BITS) {  // fp32 row partials (<= nz/kLanes voxels) -> fp64
         qx += (double)px;
         qxx += (double)pxx;
         qyx += (double)pyx;
@@ -588,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOC
   // group-ordered sum (deterministic), integer overlap count
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
-  __shared__ int cnt_w[kWarps];
+  __shared__ int cnt_w[kOctWarps];
   if (lane == 0) cnt_w[warp] = cnt;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -600,8 +634,31 @@ __global__ void __launch_bounds__(kThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOC
       out.y += gsum[q][3];
       out.yy += gsum[q][4];
     }
-    for (int w = 0; w < kWarps; ++w) out.n += cnt_w[w];
+    for (int w = 0; w < kOctWarps; ++w) out.n += cnt_w[w];
     part[slot] = out;
+  }
+}
+
+// Bit-oct re-layout of a binary source (one thread per padded cell).
+__global__ void build_bitoct_kernel(const uint8_t* __restrict__ s, int sx, int sy, int sz,
+                                    uint8_t* __restrict__ out) {
+  const int cx = sx + 1, cy = sy + 1, cz = sz + 1;
+  const long long n = (long long)cx * cy * cz;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int ck = (int)(q % cz);
+    const long long rest = q / cz;
+    const int cj = (int)(rest % cy);
+    const int ci = (int)(rest / cy);
+    const int i0 = min(max(ci - 1, 0), sx - 1), i1 = min(ci, sx - 1);
+    const int j0 = min(max(cj - 1, 0), sy - 1), j1 = min(cj, sy - 1);
+    const int k0 = min(max(ck - 1, 0), sz - 1), k1 = min(ck, sz - 1);
+    auto at = [&](int i, int j, int k) -> unsigned {
+      return s[((long long)i * sy + j) * sz + k] ? 1u : 0u;
+    };
+    out[q] = (uint8_t)(at(i0, j0, k0) | (at(i1, j0, k0) << 1) | (at(i0, j1, k0) << 2) |
+                       (at(i1, j1, k0) << 3) | (at(i0, j0, k1) << 4) | (at(i1, j0, k1) << 5) |
+                       (at(i0, j1, k1) << 6) | (at(i1, j1, k1) << 7));
   }
 }
 
@@ -771,19 +828,29 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
   cudaStream_t st = as_stream(stream);
   Partial* part = (Partial*)workspace_dev;
   // (the oct kernel's per-tile group slots assume a tile of <= kRowsPerTile rows)
-  const bool use_oct = src->oct_dev && src->dtype == ER_U8 && lerp_mode != ER_LERP_EXACT &&
-                       tgt->ny <= kRowsPerTile;
-  if (use_oct) {
+  // (the oct kernels' per-tile group slots assume a tile of <= kRowsPerTile rows)
+  const bool fast = lerp_mode != ER_LERP_EXACT && tgt->ny <= kRowsPerTile && src->dtype == ER_U8;
+  const bool use_bits = fast && lerp_mode == ER_LERP_F32 && src->bitoct_dev;
+  const bool use_oct = fast && !use_bits && src->oct_dev;
+  if (use_bits || use_oct) {
     const OctGeom og{src->ny + 1, src->nz + 1, (long long)P};
     const unsigned blocks = (unsigned)(P * g.ntiles);
-    const uint2* oct = (const uint2*)src->oct_dev;
-#define ER_OCT(TT, L) \
-  measure_oct_kernel<TT, L><<<blocks, kThreads, 0, st>>>((const TT*)tgt->data_dev, oct, A_dev, b_dev, g, og, part)
+    const uint2* lay = (const uint2*)(use_bits ? src->bitoct_dev : src->oct_dev);
+#define ER_OCT(TT, L, B) \
+  measure_oct_kernel<TT, L, B><<<blocks, kOctThreads, 0, st>>>((const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part)
     const bool f32 = lerp_mode == ER_LERP_F32;
-    switch (tgt->dtype) {
-      case ER_U8: if (f32) ER_OCT(uint8_t, ER_LERP_F32); else ER_OCT(uint8_t, ER_LERP_F64); break;
-      case ER_F32: if (f32) ER_OCT(float, ER_LERP_F32); else ER_OCT(float, ER_LERP_F64); break;
-      default: if (f32) ER_OCT(double, ER_LERP_F32); else ER_OCT(double, ER_LERP_F64); break;
+    if (use_bits) {
+      switch (tgt->dtype) {
+        case ER_U8: ER_OCT(uint8_t, ER_LERP_F32, 1); break;
+        case ER_F32: ER_OCT(float, ER_LERP_F32, 1); break;
+        default: ER_OCT(double, ER_LERP_F32, 1); break;
+      }
+    } else {
+      switch (tgt->dtype) {
+        case ER_U8: if (f32) ER_OCT(uint8_t, ER_LERP_F32, 0); else ER_OCT(uint8_t, ER_LERP_F64, 0); break;
+        case ER_F32: if (f32) ER_OCT(float, ER_LERP_F32, 0); else ER_OCT(float, ER_LERP_F64, 0); break;
+        default: if (f32) ER_OCT(double, ER_LERP_F32, 0); else ER_OCT(double, ER_LERP_F64, 0); break;
+      }
     }
 #undef ER_OCT
   } else {
@@ -817,6 +884,23 @@ extern "C" int er_build_oct(const er_volume* v, void* oct_dev, void* stream) {
   if (blocks > ER_NUM_SMS_B200 * 16) blocks = ER_NUM_SMS_B200 * 16;
   build_oct_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
       (const uint8_t*)v->data_dev, v->nx, v->ny, v->nz, (uint2*)oct_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" size_t er_bitoct_bytes(const er_volume* v) {
+  if (!v || v->nx < 1 || v->ny < 1 || v->nz < 1) return 0;
+  return (size_t)(v->nx + 1) * (size_t)(v->ny + 1) * (size_t)(v->nz + 1);
+}
+
+extern "C" int er_build_bitoct(const er_volume* v, void* bitoct_dev, void* stream) {
+  if (!valid_volume(v) || v->dtype != ER_U8 || !bitoct_dev)
+    return er_set_error(ER_EINVAL, "er_build_bitoct: needs a binary u8 volume and an output buffer");
+  const long long n = (long long)(v->nx + 1) * (v->ny + 1) * (v->nz + 1);
+  long long blocks = (n + 255) / 256;
+  if (blocks > ER_NUM_SMS_B200 * 16) blocks = ER_NUM_SMS_B200 * 16;
+  build_bitoct_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+      (const uint8_t*)v->data_dev, v->nx, v->ny, v->nz, (uint8_t*)bitoct_dev);
   ER_CHECK_LAUNCH();
   return ER_OK;
 }

@@ -101,6 +101,45 @@ class DeviceVolume:
                 sh.oct = oct_
         self.desc.oct_dev = (sh.oct if sh is not None else self.oct).data_ptr()
 
+    def stored_binary(self) -> bool:
+        """True when every stored byte is 0 or 1 (exact, from the histogram)."""
+        if self.dtype_code != _lib.ER_U8:
+            return False
+        b = getattr(self, "_binary", None)
+        if b is None:
+            b = bool(self.histogram()[2:].sum() == 0)
+            self._binary = b
+        return b
+
+    def ensure_bitoct(self):
+        """Build (once per 8-bit array) the bit-oct re-layout of a binary
+        source: the 8 corner bits of a cell in one byte (mask fast path)."""
+        if self.desc.bitoct_dev:
+            return
+        sh = self.shared
+        lay = getattr(sh, "bitoct", None) if sh is not None else getattr(self, "bitoct", None)
+        if lay is None:
+            t = torch()
+            nbytes = int(_lib.load().er_bitoct_bytes(ctypes.byref(self.desc)))
+            lay = t.empty(nbytes, dtype=t.uint8, device=self.storage.device)
+            _lib.call("er_build_bitoct", ctypes.byref(self.desc), ptr(lay),
+                      stream_ptr(self.storage.device))
+            if sh is not None:
+                sh.bitoct = lay
+            else:
+                self.bitoct = lay
+        self.desc.bitoct_dev = lay.data_ptr()
+
+    def ensure_fast_layout(self):
+        """The measurement fast-path layout for this source: bit-oct for
+        binary 8-bit data, oct for other 8-bit data."""
+        if self.dtype_code != _lib.ER_U8:
+            return
+        if self.stored_binary():
+            self.ensure_bitoct()
+        else:
+            self.ensure_oct()
+
     def histogram(self) -> np.ndarray:
         """Exact 256-bin histogram of 8-bit storage (er_histogram_u8), cached."""
         if self.dtype_code != _lib.ER_U8:
@@ -128,6 +167,7 @@ class _SharedU8:
     moments: object
     oct: object = None
     hist: object = None
+    bitoct: object = None
 
 
 _U8_STORE: dict = {}

@@ -38,7 +38,9 @@ def measure(tdv: DeviceVolume, sdv: DeviceVolume, A, B, overlap: bool, precision
     ncc, degen, n_in = out
     if P == 0:
         return ncc, degen, n_in
-    if precision != "exact":
+    if precision == "f32":
+        sdv.ensure_fast_layout()       # bit-oct for binary sources, else oct
+    elif precision == "f64":
         sdv.ensure_oct()
     need = _lib.load().er_measure_workspace_bytes(tdv.desc_ptr, P)
     ws = WORKSPACE.get(dev, need)

@@ -38,8 +38,8 @@ def test_binding_covers_header():
 
 
 def test_struct_layouts_match_header():
-    # er_volume: ptr, 4 x int32, 2 x double, ptr -> 48 bytes on LP64
-    assert ctypes.sizeof(_lib.ErVolume) == 48
+    # er_volume: ptr, 4 x int32, 2 x double, 2 x ptr -> 56 bytes on LP64
+    assert ctypes.sizeof(_lib.ErVolume) == 56
     # er_smc_ctl: 7 doubles + 2 int32
     assert ctypes.sizeof(_lib.ErSmcCtl) == 64
 
