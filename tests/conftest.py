@@ -21,6 +21,15 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    # a fresh checkout: build the sm_100a library (nvcc cross-compiles without
+    # a GPU) and the CPU oracle before any test loads them
+    from paper_2504_19930_b200 import _build
+
+    if not os.path.exists(_build.LIB):
+        _build.build()
+    from oracle import kernels as oracle_kernels
+
+    oracle_kernels.build()
 
 
 def golden(name):
