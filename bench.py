@@ -342,6 +342,8 @@ def run_ours(args):
     e2e = None
     if args.e2e_steps > 0:
         e2e = run_e2e(args, t, s, ex, dev, world)
+        if world == 1:
+            e2e["plugin_seam"] = run_plugin_seam(args, t, s, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -369,6 +371,35 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if launched:
         torch.distributed.destroy_process_group()
+
+
+def run_plugin_seam(args, t, s, dev):
+    """The reference kernel-module seam with host buffers: one
+    kernels_sm100.ncc_measure_batch call per step on the fp64 arrays the
+    reference passes (kernels_numba.py:203), i.e. both volumes uploaded as
+    fp64 and classified on the device every call, affines uploaded, results
+    read back.  No codec metadata crosses this seam, so the normalised
+    (non-integer) volumes take the generic fp64-storage kernel."""
+    import torch
+
+    from paper_2504_19930_b200 import kernels_sm100
+
+    a, b = first_iteration_affines(t, s, args.particles)
+    tgt = np.ascontiguousarray(t.data)
+    src = np.ascontiguousarray(s.data)
+    kernels_sm100.ncc_measure_batch(tgt, src, a, b, False)  # warm-up
+    times = []
+    for _ in range(max(1, args.e2e_steps)):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        z, d = kernels_sm100.ncc_measure_batch(tgt, src, a, b, False)
+        times.append(time.perf_counter() - t0)
+    sec = sum(times) / len(times)
+    return {"value": args.particles * tgt.size / sec, "unit": UNIT,
+            "h2d_bytes_per_step": int(tgt.nbytes + src.nbytes + a.nbytes + b.nbytes),
+            "d2h_bytes_per_step": int(z.nbytes + d.nbytes),
+            "step": "kernels_sm100.ncc_measure_batch on host fp64 arrays (reference "
+                    "kernel-module seam), 2000 particles"}
 
 
 def run_e2e(args, t, s, ex, dev, world):

@@ -772,6 +772,10 @@ void launch_typed(const er_volume* t, const er_volume* s, const double* A, const
 template <typename TT, typename ST>
 void launch_lerp(int lerp, const er_volume* t, const er_volume* s, const double* A,
                  const double* B, const Geom& g, Partial* part, long long P, cudaStream_t st) {
+  // fp64-stored sources lerp in fp64 even in the fp32 mode: eight F2F
+  // conversions per voxel cost more than the fp64 arithmetic (B200 fp64 is
+  // half rate), and the result is more accurate
+  if (lerp == ER_LERP_F32 && sizeof(ST) == 8) lerp = ER_LERP_F64;
   switch (lerp) {
     case ER_LERP_F32: launch_typed<TT, ST, ER_LERP_F32>(t, s, A, B, g, part, P, st); break;
     case ER_LERP_F64: launch_typed<TT, ST, ER_LERP_F64>(t, s, A, B, g, part, P, st); break;
