@@ -162,6 +162,58 @@ def c5(pmax=262144):
     return {"config": "C5 particle sweep on 256^3, 1 GPU", "rows": rows}
 
 
+def scaling(p_list=(2000, 65536), n_list=(1, 2, 4, 8), reps=5):
+    """Per-rank work of an N-GPU run, measured on this GPU: each rank runs
+    predict + update for all P particles (replicated) and affines + the
+    measurement for its shard of ceil(P/N) particles.  The NCCL all-gather of
+    P doubles is NOT measured here (one GPU); it is added as an explicit
+    estimate from the measured NVLink peer bandwidth in B200_PROFILING.md
+    (770 GB/s per direction) plus 20 us of launch latency.  A projection, not
+    a multi-GPU measurement."""
+    import bench
+    from paper_2504_19930_b200 import SmcConfig
+    from paper_2504_19930_b200 import dist, smc as dsmc
+    from paper_2504_19930_b200.backend import Executor
+
+    t, s, _ = bench.make_workload()
+    nvox = t.data.size
+    out = []
+
+    def local_gather(local, plan, dst):  # the NCCL exchange's cost is estimated below
+        dst[: plan.count].copy_(local[: plan.count])
+        return dst[: plan.n]
+
+    dsmc.dist.allgather_shards = local_gather
+    for P in p_list:
+        cfg = SmcConfig(mode="image", n_particles=P, n_iterations=reps + 2, seed=0)
+        base = None
+        for N in n_list:
+            run = dsmc.DeviceSmcRun(t, s, cfg, Executor())
+            run.plan = dist.ShardPlan(P, N, 0)  # rank 0 holds the first (largest) shard
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            for k in range(2):
+                run.step(k)
+            sync()
+            ev[0].record()
+            for k in range(2, 2 + reps):
+                run.step(k)
+            ev[1].record()
+            sync()
+            ms = ev[0].elapsed_time(ev[1]) / reps
+            gather_ms = 0.0 if N == 1 else 0.020 + P * 8 * (N - 1) / N / 770e9 * 1e3
+            it_ms = ms + gather_ms
+            evals = P * nvox / (it_ms * 1e-3)
+            if base is None:
+                base = evals
+            out.append({"particles": P, "gpus": N, "rank0_iteration_ms": round(ms, 3),
+                        "allgather_ms_estimate": round(gather_ms, 4),
+                        "projected_evals_per_s": evals, "projected_efficiency": evals / base / N})
+            print(json.dumps(out[-1]), file=sys.stderr, flush=True)
+            del run
+            torch.cuda.empty_cache()
+    return {"config": "scaling projection (per-rank work measured on one B200)", "rows": out}
+
+
 if __name__ == "__main__":
     which = [a for a in sys.argv[1:] if not a.startswith("--")] or ["c1", "c3", "c4", "c5"]
     for w in which:
