@@ -52,6 +52,13 @@ typedef struct er_volume {
 int er_abi_version(void);
 const char *er_last_error(void);
 
+/* Debug builds only (-DER_BOUNDS_CHECK=1): number of out-of-range gather
+ * indices the kernels have seen since load (each counted and clamped to 0).
+ * Returns ER_EINVAL, *count = 0, on a normal build.  No reference
+ * counterpart: this replaces compute-sanitizer memcheck, which the GPU pool
+ * does not allow. */
+int er_debug_bounds_faults(unsigned long long *count);
+
 /* ---- volumes ---------------------------------------------------------- */
 
 /* Stored-value moments: out_dev[0] = sum(stored), out_dev[1] = sum(stored^2),

@@ -62,6 +62,7 @@ _VP = ctypes.POINTER(ErVolume)
 SIGNATURES = {
     "er_abi_version": (ctypes.c_int, []),
     "er_last_error": (ctypes.c_char_p, []),
+    "er_debug_bounds_faults": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
     "er_volume_moments": (ctypes.c_int, [_VP, _p, _p]),
     "er_oct_bytes": (ctypes.c_size_t, [_VP]),
     "er_histogram_u8": (ctypes.c_int, [_VP, _p, _p]),
@@ -147,3 +148,11 @@ def d9(v) -> "ctypes.Array":
 
 def i6(v) -> "ctypes.Array":
     return _i6(*[int(x) for x in v])
+
+
+def bounds_faults():
+    """Out-of-range gather indices counted by a -DER_BOUNDS_CHECK=1 build
+    (None on a normal build, where the checks are compiled out)."""
+    n = ctypes.c_ulonglong(0)
+    rc = load().er_debug_bounds_faults(ctypes.byref(n))
+    return int(n.value) if rc == ER_OK else None

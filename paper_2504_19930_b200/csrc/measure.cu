@@ -159,11 +159,13 @@ __device__ __forceinline__ double sample(const ST* __restrict__ src, double u, d
   const int o01 = (i0 * g.sy + j1) * g.sz;
   const int o10 = (i1 * g.sy + j0) * g.sz;
   const int o11 = (i1 * g.sy + j1) * g.sz;
+  const long long ns = (long long)g.sx * g.sy * g.sz;  // er_idx extent (debug builds)
+  (void)ns;
   if (LERP == ER_LERP_F32) {
-    const float x000 = ldf(src, o00 + k0), x100 = ldf(src, o10 + k0);
-    const float x010 = ldf(src, o01 + k0), x110 = ldf(src, o11 + k0);
-    const float x001 = ldf(src, o00 + k1), x101 = ldf(src, o10 + k1);
-    const float x011 = ldf(src, o01 + k1), x111 = ldf(src, o11 + k1);
+    const float x000 = ldf(src, er_idx(o00 + k0, ns)), x100 = ldf(src, er_idx(o10 + k0, ns));
+    const float x010 = ldf(src, er_idx(o01 + k0, ns)), x110 = ldf(src, er_idx(o11 + k0, ns));
+    const float x001 = ldf(src, er_idx(o00 + k1, ns)), x101 = ldf(src, er_idx(o10 + k1, ns));
+    const float x011 = ldf(src, er_idx(o01 + k1, ns)), x111 = ldf(src, er_idx(o11 + k1, ns));
     const float a = (float)fu, b = (float)fv, c = (float)fw;
     const float c00 = fmaf(a, x100 - x000, x000);
     const float c10 = fmaf(a, x110 - x010, x010);
@@ -173,10 +175,10 @@ __device__ __forceinline__ double sample(const ST* __restrict__ src, double u, d
     const float c1 = fmaf(b, c11 - c01, c01);
     return (double)fmaf(c, c1 - c0, c0);
   } else {
-    const double x000 = ldd(src, o00 + k0), x100 = ldd(src, o10 + k0);
-    const double x010 = ldd(src, o01 + k0), x110 = ldd(src, o11 + k0);
-    const double x001 = ldd(src, o00 + k1), x101 = ldd(src, o10 + k1);
-    const double x011 = ldd(src, o01 + k1), x111 = ldd(src, o11 + k1);
+    const double x000 = ldd(src, er_idx(o00 + k0, ns)), x100 = ldd(src, er_idx(o10 + k0, ns));
+    const double x010 = ldd(src, er_idx(o01 + k0, ns)), x110 = ldd(src, er_idx(o11 + k0, ns));
+    const double x001 = ldd(src, er_idx(o00 + k1, ns)), x101 = ldd(src, er_idx(o10 + k1, ns));
+    const double x011 = ldd(src, er_idx(o01 + k1, ns)), x111 = ldd(src, er_idx(o11 + k1, ns));
     if (LERP == ER_LERP_F64) {
       const double c00 = fma(fu, x100 - x000, x000);
       const double c10 = fma(fu, x110 - x010, x010);
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         const double v = rn_add(qv, rn_mul(a12, kd));
         const double w = rn_add(qw, rn_mul(a22, kd));
         const double x = sample<ST, LERP>(src, u, v, w, g);
-        const double y = ldd(tgt, qoff + k);
+        const double y = ldd(tgt, er_idx(qoff + k, (long long)g.nx * g.ny * g.nz));
         sx += x;
         sxx = fma(x, x, sxx);
         syx = fma(y, x, syx);
@@ -442,6 +444,10 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
   const int R = (i_end - i_begin) * g.ny;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cyz = og.cy * og.cz;
+  const long long ncells = (long long)(g.sx + 1) * cyz;   // er_idx extents (debug builds)
+  const long long ntv = (long long)g.nx * g.ny * g.nz;
+  (void)ncells;
+  (void)ntv;
 
   // 32-row groups are handed out dynamically (warps whose rows are short or
   // out of bounds take more groups); each group's warp-reduced sums land in
@@ -525,8 +531,9 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
         if (BITS) {
           // binary source: one byte = the cell's 8 corner bits; uniform cells
           // (all 0 / all 1) are exact without interpolation
-          const unsigned c = __ldg(reinterpret_cast<const uint8_t*>(oct) + (unsigned)cell);
-          const float yf = ty.add(__ldg(trow + k));
+          const unsigned c = __ldg(reinterpret_cast<const uint8_t*>(oct) +
+                                   (unsigned)er_idx(cell, ncells));
+          const float yf = ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
           float x = (c == 0xFFu) ? 1.0f : 0.0f;
           if (c != 0u && c != 0xFFu) {
             const float fu = F::frac32(cu), fv = F::frac32(cv), fw = F::frac32(cw);
@@ -552,9 +559,9 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
 #if ER_OCT_TEX
         const uint2 c8 = tex1Dfetch<uint2>(otex, cell);
 #else
-        const uint2 c8 = ld_oct(oct + (unsigned)cell);
+        const uint2 c8 = ld_oct(oct + (unsigned)er_idx(cell, ncells));
 #endif
-        const float yf = ty.add(__ldg(trow + k));
+        const float yf = ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
         if (LERP == ER_LERP_F32) {
           const float fu = F::frac32(cu), fv = F::frac32(cv), fw = F::frac32(cw);
           // packed fp32x2 (FFMA2/FADD2): corners paired along k so the u-lerps
@@ -622,7 +629,7 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
     }
     if (lane == 0) {
 #pragma unroll
-      for (int c = 0; c < 5; ++c) gsum[grp][c] = v[c];
+      for (int c = 0; c < 5; ++c) gsum[er_idx(grp, kRowsPerTile / 32)][c] = v[c];
       grp = atomicAdd(&next_group, 1);
     }
     grp = __shfl_sync(0xffffffffu, grp, 0);
@@ -944,3 +951,5 @@ extern "C" int er_build_bitoct(const er_volume* v, void* bitoct_dev, void* strea
   ER_CHECK_LAUNCH();
   return ER_OK;
 }
+
+ER_DEFINE_FAULT_READER(er_faults_measure)

@@ -479,3 +479,5 @@ extern "C" int er_smc_update(const double* z_dev, const uint8_t* degen_dev, doub
   ER_CHECK_LAUNCH();
   return ER_OK;
 }
+
+ER_DEFINE_FAULT_READER(er_faults_smc)

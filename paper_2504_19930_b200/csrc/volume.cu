@@ -193,3 +193,5 @@ extern "C" int er_histogram_u8(const er_volume* v, int64_t* hist_dev, void* stre
   ER_CHECK_LAUNCH();
   return ER_OK;
 }
+
+ER_DEFINE_FAULT_READER(er_faults_volume)

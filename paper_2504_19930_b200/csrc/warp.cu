@@ -58,11 +58,13 @@ __device__ __forceinline__ double warp_value(const ST* __restrict__ src, const W
   cell(w, g.sz, k0, k1, fw);
   const long long o00 = ((long long)i0 * g.sy + j0) * g.sz, o01 = ((long long)i0 * g.sy + j1) * g.sz;
   const long long o10 = ((long long)i1 * g.sy + j0) * g.sz, o11 = ((long long)i1 * g.sy + j1) * g.sz;
+  const long long ns = (long long)g.sx * g.sy * g.sz;  // er_idx extent (debug builds)
+  (void)ns;
   const double gu = rn_sub(1.0, fu), gv = rn_sub(1.0, fv), gw = rn_sub(1.0, fw);
-  const double c00 = rn_add(rn_mul(ld(src, o00 + k0), gu), rn_mul(ld(src, o10 + k0), fu));
-  const double c10 = rn_add(rn_mul(ld(src, o01 + k0), gu), rn_mul(ld(src, o11 + k0), fu));
-  const double c01 = rn_add(rn_mul(ld(src, o00 + k1), gu), rn_mul(ld(src, o10 + k1), fu));
-  const double c11 = rn_add(rn_mul(ld(src, o01 + k1), gu), rn_mul(ld(src, o11 + k1), fu));
+  const double c00 = rn_add(rn_mul(ld(src, er_idx(o00 + k0, ns)), gu), rn_mul(ld(src, er_idx(o10 + k0, ns)), fu));
+  const double c10 = rn_add(rn_mul(ld(src, er_idx(o01 + k0, ns)), gu), rn_mul(ld(src, er_idx(o11 + k0, ns)), fu));
+  const double c01 = rn_add(rn_mul(ld(src, er_idx(o00 + k1, ns)), gu), rn_mul(ld(src, er_idx(o10 + k1, ns)), fu));
+  const double c11 = rn_add(rn_mul(ld(src, er_idx(o01 + k1, ns)), gu), rn_mul(ld(src, er_idx(o11 + k1, ns)), fu));
   const double c0 = rn_add(rn_mul(c00, gv), rn_mul(c10, fv));
   const double c1 = rn_add(rn_mul(c01, gv), rn_mul(c11, fv));
   const double x = rn_add(rn_mul(c0, gw), rn_mul(c1, fw));
@@ -301,3 +303,5 @@ extern "C" int er_warp_ncc_sums(const er_volume* tgt, const er_volume* src, cons
   ER_CHECK_LAUNCH();
   return ER_OK;
 }
+
+ER_DEFINE_FAULT_READER(er_faults_warp)

@@ -58,3 +58,16 @@ def have_gpu():
         return torch.cuda.is_available()
     except Exception:  # pragma: no cover
         return False
+
+
+@pytest.fixture(autouse=True)
+def _no_bounds_faults(request):
+    """Under tools/bounds_check.sh (a -DER_BOUNDS_CHECK=1 build), fail the GPU
+    test during which any kernel saw an out-of-range gather index."""
+    yield
+    if os.environ.get("ER_ASSERT_NO_BOUNDS_FAULTS") and request.node.get_closest_marker("gpu"):
+        from paper_2504_19930_b200 import _lib
+
+        faults = _lib.bounds_faults()
+        assert faults is not None, "ER_ASSERT_NO_BOUNDS_FAULTS set on a build without checks"
+        assert faults == 0, f"{faults} out-of-range gather indices"

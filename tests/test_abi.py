@@ -50,6 +50,13 @@ def test_abi_version_and_error_text_without_gpu():
     assert isinstance(lib.er_last_error(), bytes)
 
 
+def test_bounds_checks_compiled_out_of_the_normal_build():
+    if "ER_BOUNDS_CHECK" in os.environ.get("ER_NVCC_EXTRA", ""):
+        pytest.skip("debug build")
+    assert _lib.bounds_faults() is None
+    assert b"ER_BOUNDS_CHECK" in _lib.load().er_last_error()
+
+
 def test_sass_is_sm100a():
     """The library carries sm_100a SASS (cuobjdump), not PTX-only or another arch."""
     import shutil
