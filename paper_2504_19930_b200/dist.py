@@ -67,3 +67,25 @@ def allgather_shards(local, plan: ShardPlan, out):
         return out[: plan.n]
     td.all_gather_into_tensor(out, local)
     return out[: plan.n]
+
+
+def allgather_rows(local, plan: ShardPlan):
+    """Gather every rank's padded (plan.shard, k) float64 block of host rows
+    (numpy) and return the first plan.n rows, in rank order.  Used for the
+    per-frame scores of the 4D pipeline: small, so the
+    exchange goes through the default group's device (NCCL: the current CUDA
+    device; gloo: host memory)."""
+    import numpy as np
+
+    local = np.ascontiguousarray(local, dtype=np.float64)
+    if plan.world == 1:
+        return local[: plan.n].copy()
+    import torch
+    import torch.distributed as td
+
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if td.get_backend() == "nccl" else torch.device("cpu")
+    src = torch.from_numpy(local).to(dev).reshape(-1)
+    out = torch.empty(src.numel() * plan.world, dtype=torch.float64, device=dev)
+    td.all_gather_into_tensor(out, src)
+    return out.cpu().numpy().reshape(plan.world * plan.shard, -1)[: plan.n]

@@ -125,3 +125,62 @@ def test_sharded_smc_and_grid_bit_identical(world):
         assert np.array_equal(z, np.stack(tr1.z)), rank
         assert resampled == tr1.resampled
         assert bi == 17                                # lowest index wins the tie
+
+
+def _frames_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2504_19930_b200 import errors, pipeline
+
+        seen = []
+
+        def scorer(tgt, src, tm, sm, matrix):  # stands in for the device warp + scores
+            seen.append(tgt)
+            if tgt == 6 and matrix is None:
+                raise errors.DegenerateInput("constant")
+            has = tm is not None and sm is not None
+            return [tgt + 0.5, -tgt, float(has), tgt * 0.01 if has else 0.0, 0.3, 0.0]
+
+        frames = list(range(7))
+        masks = [1, None, 1, 1, None, 1, 1]
+        res = pipeline.score_frames(frames, frames, masks, masks, np.eye(4), scorer=scorer)
+        try:
+            pipeline.score_frames(frames, frames, masks, masks, None, scorer=scorer)
+            raised = None
+        except errors.DegenerateInput as e:
+            raised = str(e)
+        out_q.put((rank, res, seen, raised))
+    finally:
+        td.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_score_frames_sharded_over_ranks(world):
+    """The 4D scoring shards frames (contiguous ranges) and all-gathers the
+    per-frame rows: every rank returns the full lists, in frame order, with
+    None DSC for mask-less frames; a degenerate frame on one rank raises on
+    all of them instead of leaving the others in the collective."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_frames_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect_b = [f + 0.5 for f in range(7)]
+    expect_dsc = [None if f in (1, 4) else f * 0.01 for f in range(7)]
+    owned = []
+    for rank, (nb, na, db, da), seen, raised in results:
+        assert nb == expect_b and na == [-float(f) for f in range(7)]
+        assert db == expect_dsc
+        assert da == [None if f in (1, 4) else 0.3 for f in range(7)]
+        plan = dist.ShardPlan(7, world, rank)
+        assert seen[: plan.count] == list(range(plan.lo, plan.hi))
+        owned += seen[: plan.count]
+        assert raised is not None and "frame 6" in raised
+    assert sorted(owned) == list(range(7))
