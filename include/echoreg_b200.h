@@ -188,6 +188,38 @@ int er_warp_dice_counts(const er_volume *src_mask, const double A[9], const doub
 int er_warp_ncc_sums(const er_volume *tgt, const er_volume *src, const double A[9],
                      const double b[3], int32_t identity, double *out_dev, void *stream);
 
+/* ---- synthetic phantoms (E/phantom.py:61-91) ------- */
+
+/* Device scratch needed by er_phantom_speckle for n voxels. */
+size_t er_phantom_scratch_bytes(int64_t n);
+
+/* speckle_out[i] = np.exp(sigma * z_i), z = Generator(Philox(key=seed))
+ * .standard_normal(n) (E/phantom.py:76-77), bit-exact: the ziggurat's
+ * variable word consumption is resolved in parallel (chunked chain walk) and
+ * exp is numpy's AVX512 SVML exp restated (csrc/npexp.cuh).  normals_out
+ * (optional) receives z.  Synchronises the stream (checks the chain). */
+int er_phantom_speckle(uint64_t seed, int64_t n, double sigma, void *scratch_dev,
+                       size_t scratch_bytes, double *speckle_out_dev, double *normals_out_dev,
+                       void *stream);
+
+/* One frame of make_phantom (E/phantom.py:78-90): base intensity from the two
+ * ellipsoid radii (semi-axes already scaled for the frame, as the reference
+ * computes them) times the speckle -> frame_out (optional); cavity -> mask_out
+ * bytes (optional).  C-order (nx, ny, nz), fp64 in the reference's op order. */
+int er_phantom_frame(const double *speckle_dev, int32_t nx, int32_t ny, int32_t nz,
+                     const double spacing[3], const double center[3], const double outer[3],
+                     const double inner[3], double *frame_out_dev, uint8_t *mask_out_dev,
+                     void *stream);
+
+/* out = clip(round_half_even(v * scale), 0, 255) as bytes; entries at index
+ * >= keep_before are 0 (make_pair's overlap crop, E/phantom.py:139-145). */
+int er_quantize_u8(const double *v_dev, int64_t n, double scale, int64_t keep_before,
+                   uint8_t *out_dev, void *stream);
+
+/* out = (v > threshold) as bytes (E/volume.py:133-135), 0 at index >= keep_before. */
+int er_binarize_u8(const double *v_dev, int64_t n, double threshold, int64_t keep_before,
+                   uint8_t *out_dev, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,11 @@ SIGNATURES = {
     "er_resample": (ctypes.c_int, [_VP, _d9, _d3, _i32, _i32, _i32, _p, _p]),
     "er_warp_dice_counts": (ctypes.c_int, [_VP, _d9, _d3, _VP, _p, _p]),
     "er_warp_ncc_sums": (ctypes.c_int, [_VP, _VP, _d9, _d3, _i32, _p, _p]),
+    "er_phantom_scratch_bytes": (ctypes.c_size_t, [_i64]),
+    "er_phantom_speckle": (ctypes.c_int, [_u64, _i64, _f64, _p, ctypes.c_size_t, _p, _p, _p]),
+    "er_phantom_frame": (ctypes.c_int, [_p, _i32, _i32, _i32, _d3, _d3, _d3, _d3, _p, _p, _p]),
+    "er_quantize_u8": (ctypes.c_int, [_p, _i64, _f64, _i64, _p, _p]),
+    "er_binarize_u8": (ctypes.c_int, [_p, _i64, _f64, _i64, _p, _p]),
 }
 
 _lib = None
@@ -95,7 +100,8 @@ LAUNCHES_PER_CALL = {
     "er_volume_moments": 2, "er_classify_f64": 2, "er_build_oct": 1, "er_build_bitoct": 1, "er_histogram_u8": 2, "er_convert_f64": 1, "er_measure_ncc": 2,
     "er_smc_init": 1, "er_smc_predict": 1, "er_states_to_affine": 1, "er_grid_to_affine": 1,
     "er_argmax_update": 1, "er_smc_update": 1, "er_resample": 1, "er_warp_dice_counts": 2,
-    "er_warp_ncc_sums": 4,
+    "er_warp_ncc_sums": 4, "er_phantom_speckle": 5, "er_phantom_frame": 1, "er_quantize_u8": 1,
+    "er_binarize_u8": 1,
 }
 launch_count = 0
 

@@ -25,7 +25,8 @@ extern "C" const char* er_last_error(void) { return g_last_error; }
 
 extern "C" int er_debug_bounds_faults(unsigned long long* count) {
   if (!count) return er_set_error(ER_EINVAL, "er_debug_bounds_faults: null count");
-  *count = er_faults_measure() + er_faults_warp() + er_faults_volume() + er_faults_smc();
+  *count = er_faults_measure() + er_faults_warp() + er_faults_volume() + er_faults_smc() +
+           er_faults_phantom();
   return ER_BOUNDS_CHECK ? ER_OK : er_set_error(ER_EINVAL,
                                                  "er_debug_bounds_faults: library built "
                                                  "without -DER_BOUNDS_CHECK=1");

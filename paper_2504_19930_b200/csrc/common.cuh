@@ -62,5 +62,6 @@ unsigned long long er_faults_measure();
 unsigned long long er_faults_warp();
 unsigned long long er_faults_volume();
 unsigned long long er_faults_smc();
+unsigned long long er_faults_phantom();
 
 constexpr int ER_NUM_SMS_B200 = 148;

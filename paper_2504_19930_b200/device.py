@@ -311,3 +311,40 @@ def u8_histogram(raw: np.ndarray, device=None) -> np.ndarray:
         _lib.call("er_histogram_u8", ctypes.byref(desc), ptr(h), stream_ptr(dev))
         sh.hist = h.cpu().numpy()
     return sh.hist
+
+
+def adopt_u8(raw: np.ndarray, storage, device=None) -> _SharedU8:
+    """Register a u8 tensor already resident on the device as the upload of
+    the host array ``raw`` (same bytes), so volumes built on ``raw`` never
+    re-upload it (device-generated phantoms)."""
+    import weakref
+
+    dev = require_cuda(device)
+    key = (id(raw), dev.index)
+    desc = _make_desc(storage, _lib.ER_U8, raw.shape, 1.0, 0.0)
+    t = torch()
+    moments = t.empty(_lib.ER_MOMENTS_DOUBLES, dtype=t.float64, device=dev)
+    _lib.call("er_volume_moments", ctypes.byref(desc), ptr(moments), stream_ptr(dev))
+    ref = weakref.ref(raw, lambda _r, k=key: _U8_STORE.pop(k, None))
+    sh = _SharedU8(ref, storage.reshape(-1), moments)
+    _U8_STORE[key] = sh
+    return sh
+
+
+def adopt_f64(v, storage, device=None) -> DeviceVolume:
+    """Attach a resident fp64 tensor (same values as ``v.data``) as the device
+    copy of the fp64 volume ``v``."""
+    dev = require_cuda(device)
+    t = torch()
+    flat = storage.reshape(-1)
+    desc = _make_desc(flat, _lib.ER_F64, v.dims, 1.0, 0.0)
+    moments = t.empty(_lib.ER_MOMENTS_DOUBLES, dtype=t.float64, device=dev)
+    _lib.call("er_volume_moments", ctypes.byref(desc), ptr(moments), stream_ptr(dev))
+    dv = DeviceVolume(flat, desc, tuple(v.dims), tuple(v.spacing), tuple(v.origin), moments,
+                      _lib.ER_F64)
+    cache = getattr(v, "_er_device_cache", None)
+    if cache is None:
+        cache = {}
+        object.__setattr__(v, "_er_device_cache", cache)
+    cache[dev.index] = dv
+    return dv

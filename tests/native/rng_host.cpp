@@ -17,3 +17,7 @@ extern "C" void er_host_uniforms(uint64_t seed, uint64_t role, uint64_t step, ui
   er_stream_init(&s, seed, role, step, index);
   for (int64_t i = 0; i < n; ++i) out[i] = er_uniform(&s, lo, range);
 }
+
+extern "C" void er_host_log1p(const double* x, double* out, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) out[i] = er_log1p(x[i]);
+}

@@ -75,3 +75,44 @@ def test_uniform_matches_numpy(lib):
     lib.er_host_uniforms(123, 4, 5, 6, 50, -2.0, 5.0,
                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     assert np.array_equal(out, want)
+
+
+def _host_has_fma():
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:  # pragma: no cover
+        return False
+    return " fma " in flags and " avx2 " in flags
+
+
+@pytest.mark.skipif(not _host_has_fma(), reason="glibc picks its FMA log1p only on FMA hosts")
+def test_log1p_is_glibcs(lib):
+    """er_log1p (the ziggurat tail's log1p, whose value is returned) equals
+    the host's glibc log1p -- what numpy's npy_log1p calls -- bit for bit on
+    the tail's arguments -u, u in [0, 1), and across the other branches."""
+    import math
+
+    lib.er_host_log1p.argtypes = [ctypes.POINTER(ctypes.c_double)] * 2 + [ctypes.c_int64]
+    g = np.random.default_rng(5)
+    u = (g.integers(0, 2**53, 400_000, dtype=np.int64) * 2.0**-53)
+    x = np.concatenate([-u, g.uniform(-1, 4, 100_000), g.uniform(-1e-6, 1e-6, 20_000),
+                        10.0 ** g.uniform(-30, 300, 20_000), -(2.0 ** -np.arange(1, 60)),
+                        [0.0, -0.0, 1e-300, -1e-300, 5e-324, 1.0, 0.41421, -0.29289, 1e300]])
+    y = np.empty_like(x)
+    d = ctypes.POINTER(ctypes.c_double)
+    lib.er_host_log1p(x.ctypes.data_as(d), y.ctypes.data_as(d), x.size)
+    want = np.array([math.log1p(v) for v in x])
+    bad = np.flatnonzero(y.view(np.uint64) != want.view(np.uint64))
+    assert bad.size == 0, (x[bad[:5]], y[bad[:5]], want[bad[:5]])
+
+
+@pytest.mark.parametrize("seed,n", [(0, 262144), (11, 8712), (7, 1_000_000)])
+def test_phantom_stream_normals_bit_exact(lib, seed, n):
+    """Philox(key=seed).standard_normal(n) -- the phantom speckle's stream
+    (E/phantom.py:76-77), counter 0 = stream (seed, 0, 0, 0) -- incl. its
+    ~0.03% tail draws."""
+    want = np.random.Generator(np.random.Philox(key=seed)).standard_normal(n)
+    got = normals(lib, seed, 0, 0, 0, n)
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, (bad[:5], got[bad[:5]], want[bad[:5]])
+    assert (np.abs(want) > 3.6541528853610087).sum() > 0

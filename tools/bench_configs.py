@@ -83,10 +83,10 @@ def c1(cpu=False):
 
 def c3():
     from paper_2504_19930_b200 import Executor, SmcConfig, register_sequence
-    from paper_2504_19930_b200.phantom import echo_case
+    from paper_2504_19930_b200.phantom_device import echo_case_device
 
     t0 = time.perf_counter()
-    case = echo_case(frames=30, seed=0)
+    case = echo_case_device(frames=30, seed=0)
     gen_s = time.perf_counter() - t0
     cfg = SmcConfig(mode="mask", n_particles=2000, n_iterations=50, seed=0)
     # warm-up on a 2-frame slice
@@ -132,9 +132,9 @@ def c5(pmax=262144):
     from paper_2504_19930_b200 import SmcConfig, Volume3, normalize_zscore, ops
     from paper_2504_19930_b200 import smc as dsmc
     from paper_2504_19930_b200.backend import Executor
-    from paper_2504_19930_b200.phantom import echo_case
+    from paper_2504_19930_b200.phantom_device import echo_case_device
 
-    case = echo_case(dims=(256, 256, 256), spacing=(0.8, 0.8, 0.8), frames=1, seed=0)
+    case = echo_case_device(dims=(256, 256, 256), spacing=(0.8, 0.8, 0.8), frames=1, seed=0)
     t = normalize_zscore(case.target.frames[0])
     s = normalize_zscore(case.source.frames[0])
     rows = []
