@@ -47,7 +47,6 @@ typedef struct er_volume {
   double alpha, gamma;  /* value = alpha * stored + gamma */
   const void *oct_dev;  /* optional er_build_oct() re-layout of a u8 volume, or NULL */
   const void *bitoct_dev; /* optional er_build_bitoct() re-layout of a binary volume */
-  const void *rowsum_dev; /* optional er_build_rowsum() row prefix sums of a u8 target */
 } er_volume;
 
 int er_abi_version(void);
@@ -83,15 +82,6 @@ int er_build_oct(const er_volume *v, void *oct_dev, void *stream);
  * the mask fast path (1-byte gathers; uniform cells skip the lerps). */
 size_t er_bitoct_bytes(const er_volume *v);
 int er_build_bitoct(const er_volume *v, void *bitoct_dev, void *stream);
-
-/* Row prefix sums of a u8 volume used as a measurement TARGET: entry
- * (i, j, k), k = 0..nz, holds (sum, sum of squares) of stored bytes
- * [i, j, 0..k) as two uint32 (exact).  A particle's in-bounds voxels of a
- * target row form one k-interval (kernels_numba.py:148-157), so its target
- * sums are two lookups per row instead of two integer ops per voxel.
- * er_rowsum_bytes() = nx*ny*(nz+1)*8.  Set er_volume.rowsum_dev to enable. */
-size_t er_rowsum_bytes(const er_volume *v);
-int er_build_rowsum(const er_volume *v, void *rowsum_dev, void *stream);
 
 /* 256-bin histogram of a u8 volume (exact int64 counts, order-free integer
  * atomics): the z-score of volume.py:119-130 on 8-bit data is computed from

@@ -19,7 +19,7 @@ int er_set_cuda_error(cudaError_t e, const char* where) {
   return ER_ECUDA;
 }
 
-extern "C" int er_abi_version(void) { return 2; }  // 2: er_volume.rowsum_dev
+extern "C" int er_abi_version(void) { return 1; }
 
 extern "C" const char* er_last_error(void) { return g_last_error; }
 

@@ -417,14 +417,12 @@ struct OctGeom {
 
 // BITS = 1: `oct` points at the bit-oct layout of a binary source (1 byte per
 // cell) and the lerps run in fp32 (row partials folded per row as below).
-// RS = 1 (u8 targets): the target sums of a row's in-bounds k-run come from
-// the er_build_rowsum prefix table (two lookups per row), not from the voxel loop.
-template <typename TT, int LERP, int BITS = 0, int RS = 0>
+template <typename TT, int LERP, int BITS = 0>
 __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOCKS_F32 : 3)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
                        const OctGeom og, Partial* __restrict__ part,
-                       cudaTextureObject_t otex, const uint2* __restrict__ rowsum) {
+                       cudaTextureObject_t otex) {
   using F = Fix<LERP == ER_LERP_F32 ? 32 : 40>;
 #if ER_OCT_TILE_MAJOR
   // tile-major launch order: the CTAs resident at any moment work on the same
@@ -475,12 +473,11 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
 
   for (int grp = warp; grp < ngroups;) {
     const int r = grp * 32 + lane;
-    int klo = 0, khi = 0, off = 0, rowi = 0;
+    int klo = 0, khi = 0, off = 0;
     double u0 = 0.0, v0 = 0.0, w0 = 0.0;
     if (r < R) {
       const int i = i_begin + r / g.ny;
       const int j = r - (r / g.ny) * g.ny;
-      rowi = i * g.ny + j;
       const double di = (double)i, dj = (double)j;
       u0 = rn_add(rn_add(rn_mul(sab[0], di), rn_mul(sab[1], dj)), sab[9]);
       v0 = rn_add(rn_add(rn_mul(sab[3], di), rn_mul(sab[4], dj)), sab[10]);
@@ -497,14 +494,6 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
     TgtAcc<TT> ty;
     float px = 0.f, pxx = 0.f, pyx = 0.f;
     double qx = 0.0, qxx = 0.0, qyx = 0.0;
-    if constexpr (RS != 0) {
-      if (khi > klo) {  // exact u32 row sums of the in-bounds k-run
-        const uint2* rs = rowsum + (long long)rowi * (g.nz + 1);
-        const uint2 a = __ldg(rs + klo), b = __ldg(rs + khi);
-        ty.y += b.x - a.x;
-        ty.yy += b.y - a.y;
-      }
-    }
     constexpr bool kSmemAcc = ER_OCT_SMEM_ACC && (LERP == ER_LERP_F32 || BITS);
     if (kSmemAcc) racc[threadIdx.x] = make_double3(0.0, 0.0, 0.0);
     // row start in fixed point (per lane: its own row)
@@ -556,8 +545,7 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
           // (all 0 / all 1) are exact without interpolation
           const unsigned c = __ldg(reinterpret_cast<const uint8_t*>(oct) +
                                    (unsigned)er_idx(cell, ncells));
-          const float yf = RS ? (float)__ldg(tgt + er_idx(trow - tgt + k, ntv))
-                             : ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
+          const float yf = ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
           float x = (c == 0xFFu) ? 1.0f : 0.0f;
           if (c != 0u && c != 0xFFu) {
             const float fu = F::frac32(cu), fv = F::frac32(cv), fw = F::frac32(cw);
@@ -585,8 +573,7 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
 #else
         const uint2 c8 = ld_oct(oct + (unsigned)er_idx(cell, ncells));
 #endif
-        const float yf = RS ? (float)__ldg(tgt + er_idx(trow - tgt + k, ntv))
-                             : ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
+        const float yf = ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
         if (LERP == ER_LERP_F32) {
 #if ER_OCT_FMUL2
           const float2 fuv = __fmul2_rn(make_float2(__uint2float_rz((unsigned)cu),
@@ -702,23 +689,6 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
 }
 
 // Bit-oct re-layout of a binary source (one thread per padded cell).
-// one thread per target row: exclusive prefix (sum, sum of squares), exact
-__global__ void build_rowsum_kernel(const uint8_t* __restrict__ v, long long rows, int nz,
-                                    uint2* __restrict__ out) {
-  const long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (row >= rows) return;
-  const uint8_t* src = v + row * nz;
-  uint2* dst = out + row * (nz + 1);
-  unsigned s = 0, ss = 0;
-  dst[0] = make_uint2(0u, 0u);
-  for (int k = 0; k < nz; ++k) {
-    const unsigned b = src[k];
-    s += b;
-    ss += b * b;
-    dst[k + 1] = make_uint2(s, ss);
-  }
-}
-
 __global__ void build_bitoct_kernel(const uint8_t* __restrict__ s, int sx, int sy, int sz,
                                     uint8_t* __restrict__ out) {
   const int cx = sx + 1, cy = sy + 1, cz = sz + 1;
@@ -947,29 +917,23 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
 #if ER_OCT_TEX
     if (!use_bits) otex = oct_texture(lay, (size_t)(src->nx + 1) * (src->ny + 1) * (src->nz + 1));
 #endif
-    const uint2* rsum = (const uint2*)tgt->rowsum_dev;
-#define ER_OCT_RS(TT, L, B, RSV) \
-  measure_oct_kernel<TT, L, B, RSV><<<blocks, kOctThreads, 0, st>>>((const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part, otex, rsum)
-#define ER_OCT(TT, L, B) ER_OCT_RS(TT, L, B, 0)
-#define ER_OCT_U8(L, B) \
-  do { if (rsum) ER_OCT_RS(uint8_t, L, B, 1); else ER_OCT_RS(uint8_t, L, B, 0); } while (0)
+#define ER_OCT(TT, L, B) \
+  measure_oct_kernel<TT, L, B><<<blocks, kOctThreads, 0, st>>>((const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part, otex)
     const bool f32 = lerp_mode == ER_LERP_F32;
     if (use_bits) {
       switch (tgt->dtype) {
-        case ER_U8: ER_OCT_U8(ER_LERP_F32, 1); break;
+        case ER_U8: ER_OCT(uint8_t, ER_LERP_F32, 1); break;
         case ER_F32: ER_OCT(float, ER_LERP_F32, 1); break;
         default: ER_OCT(double, ER_LERP_F32, 1); break;
       }
     } else {
       switch (tgt->dtype) {
-        case ER_U8: if (f32) ER_OCT_U8(ER_LERP_F32, 0); else ER_OCT_U8(ER_LERP_F64, 0); break;
+        case ER_U8: if (f32) ER_OCT(uint8_t, ER_LERP_F32, 0); else ER_OCT(uint8_t, ER_LERP_F64, 0); break;
         case ER_F32: if (f32) ER_OCT(float, ER_LERP_F32, 0); else ER_OCT(float, ER_LERP_F64, 0); break;
         default: if (f32) ER_OCT(double, ER_LERP_F32, 0); else ER_OCT(double, ER_LERP_F64, 0); break;
       }
     }
 #undef ER_OCT
-#undef ER_OCT_U8
-#undef ER_OCT_RS
   } else {
     switch (tgt->dtype) {
       case ER_U8: launch_src<uint8_t>(lerp_mode, tgt, src, A_dev, b_dev, g, part, P, st); break;
@@ -1001,23 +965,6 @@ extern "C" int er_build_oct(const er_volume* v, void* oct_dev, void* stream) {
   if (blocks > ER_NUM_SMS_B200 * 16) blocks = ER_NUM_SMS_B200 * 16;
   build_oct_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
       (const uint8_t*)v->data_dev, v->nx, v->ny, v->nz, (uint2*)oct_dev);
-  ER_CHECK_LAUNCH();
-  return ER_OK;
-}
-
-extern "C" size_t er_rowsum_bytes(const er_volume* v) {
-  if (!v || v->nx < 1 || v->ny < 1 || v->nz < 1) return 0;
-  return (size_t)v->nx * (size_t)v->ny * (size_t)(v->nz + 1) * sizeof(uint2);
-}
-
-extern "C" int er_build_rowsum(const er_volume* v, void* rowsum_dev, void* stream) {
-  if (!valid_volume(v) || v->dtype != ER_U8 || !rowsum_dev)
-    return er_set_error(ER_EINVAL, "er_build_rowsum: needs a u8 volume and an output buffer");
-  if ((long long)v->nz * 65025LL >= (1LL << 32))
-    return er_set_error(ER_EINVAL, "er_build_rowsum: rows too long for uint32 sums");
-  const long long rows = (long long)v->nx * v->ny;
-  build_rowsum_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, as_stream(stream)>>>(
-      (const uint8_t*)v->data_dev, rows, v->nz, (uint2*)rowsum_dev);
   ER_CHECK_LAUNCH();
   return ER_OK;
 }

@@ -130,26 +130,6 @@ class DeviceVolume:
                 self.bitoct = lay
         self.desc.bitoct_dev = lay.data_ptr()
 
-    def ensure_rowsum(self):
-        """Build (once per 8-bit array) the row prefix sums used when this
-        volume is a measurement TARGET (er_build_rowsum): the in-bounds target
-        sums become two lookups per row instead of work per voxel."""
-        if self.dtype_code != _lib.ER_U8 or self.desc.rowsum_dev:
-            return
-        sh = self.shared
-        lay = getattr(sh, "rowsum", None) if sh is not None else getattr(self, "rowsum", None)
-        if lay is None:
-            t = torch()
-            nbytes = int(_lib.load().er_rowsum_bytes(ctypes.byref(self.desc)))
-            lay = t.empty(nbytes, dtype=t.uint8, device=self.storage.device)
-            _lib.call("er_build_rowsum", ctypes.byref(self.desc), ptr(lay),
-                      stream_ptr(self.storage.device))
-            if sh is not None:
-                sh.rowsum = lay
-            else:
-                self.rowsum = lay
-        self.desc.rowsum_dev = lay.data_ptr()
-
     def ensure_fast_layout(self):
         """The measurement fast-path layout for this source: bit-oct for
         binary 8-bit data, oct for other 8-bit data."""
@@ -188,7 +168,6 @@ class _SharedU8:
     oct: object = None
     hist: object = None
     bitoct: object = None
-    rowsum: object = None
 
 
 _U8_STORE: dict = {}

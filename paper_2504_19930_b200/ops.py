@@ -40,10 +40,8 @@ def measure(tdv: DeviceVolume, sdv: DeviceVolume, A, B, overlap: bool, precision
         return ncc, degen, n_in
     if precision == "f32":
         sdv.ensure_fast_layout()       # bit-oct for binary sources, else oct
-        tdv.ensure_rowsum()            # u8 targets: row prefix sums
     elif precision == "f64":
         sdv.ensure_oct()
-        tdv.ensure_rowsum()
     need = _lib.load().er_measure_workspace_bytes(tdv.desc_ptr, P)
     ws = WORKSPACE.get(dev, need)
     _lib.call("er_measure_ncc", tdv.desc_ptr, sdv.desc_ptr, ptr(tdv.moments), ptr(A), ptr(B),
