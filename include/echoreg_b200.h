@@ -93,6 +93,18 @@ int er_histogram_u8(const er_volume *v, int64_t *hist_dev, void *stream);
  * representable in fp32.  Used to pick a lossless storage type. */
 int er_classify_f64(const double *data_dev, int64_t n, int32_t *flags_dev, void *stream);
 
+/* out2_dev[0] = min, out2_dev[1] = max of an f64 array (NaN-free), exact. */
+int er_minmax_f64(const double *data_dev, int64_t n, double *out2_dev, void *stream);
+
+/* Recover 8-bit data behind an affine image (e.g. the reference's z-score of
+ * 8-bit echo data, volume.py:119-130, which reaches the kernel-module seam as
+ * plain fp64): out_dev[i] = rint((x_i - x0) / delta); flag_dev[0] (int32)
+ * stays 1 iff every byte is in 0..255 and |x_i - (x0 + k_i delta)| <= tol.
+ * The volume can then be measured as u8 storage with alpha = delta,
+ * gamma = x0 (the oct fast path) -- values reproduced to <= tol. */
+int er_lattice_u8(const double *data_dev, int64_t n, double x0, double delta, double tol,
+                  uint8_t *out_dev, int32_t *flag_dev, void *stream);
+
 /* Convert an f64 volume to u8 (values must be integers 0..255) or f32. */
 int er_convert_f64(const double *data_dev, int64_t n, int32_t dst_dtype, void *dst_dev,
                    void *stream);

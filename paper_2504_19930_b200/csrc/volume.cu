@@ -120,6 +120,64 @@ __global__ void zero_u64_kernel(unsigned long long* p, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
 }
 
+// order-preserving map of a (non-NaN) double onto uint64, for atomic min/max
+__device__ __forceinline__ unsigned long long ord_u64(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double unord_u64(unsigned long long u) {
+  return __longlong_as_double((long long)((u >> 63) ? (u & 0x7fffffffffffffffULL) : ~u));
+}
+
+__global__ void minmax_init_kernel(unsigned long long* mm) {
+  mm[0] = ~0ULL;  // running min (ordered)
+  mm[1] = 0ULL;   // running max (ordered)
+}
+
+__global__ void minmax_kernel(const double* __restrict__ v, long long n,
+                              unsigned long long* __restrict__ mm) {
+  unsigned long long lo = ~0ULL, hi = 0ULL;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long o = ord_u64(__ldg(v + q));
+    lo = min(lo, o);
+    hi = max(hi, o);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    lo = min(lo, __shfl_down_sync(0xffffffffu, lo, off));
+    hi = max(hi, __shfl_down_sync(0xffffffffu, hi, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+  }
+}
+
+__global__ void minmax_final_kernel(unsigned long long* mm) {
+  double* d = reinterpret_cast<double*>(mm);
+  const double a = unord_u64(mm[0]), b = unord_u64(mm[1]);
+  d[0] = a;
+  d[1] = b;
+}
+
+// stored byte k = rint((x - x0) / delta), valid iff 0 <= k <= 255 and
+// |x - (x0 + k delta)| <= tol for every voxel (flags[0] cleared otherwise)
+__global__ void lattice_kernel(const double* __restrict__ v, long long n, double x0, double delta,
+                               double tol, uint8_t* __restrict__ out, int* __restrict__ flags) {
+  bool ok = true;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const double x = __ldg(v + q);
+    const double k = rint(__ddiv_rn(__dsub_rn(x, x0), delta));
+    const bool in = (k >= 0.0) & (k <= 255.0) &
+                    (fabs(__dsub_rn(x, __dadd_rn(x0, __dmul_rn(k, delta)))) <= tol);
+    ok &= in;
+    out[q] = in ? (uint8_t)k : 0;
+  }
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicAnd(flags, 0);
+}
+
 template <typename T>
 void launch_moments(const void* data, long long n, double* part, cudaStream_t st) {
   moments_partial_kernel<T><<<kMomBlocks, kMomThreads, 0, st>>>((const T*)data, n, part);
@@ -171,6 +229,35 @@ extern "C" int er_convert_f64(const double* data_dev, int64_t n, int32_t dst_dty
     case ER_U8: convert_kernel<uint8_t><<<(unsigned)blocks, 256, 0, st>>>(data_dev, n, (uint8_t*)dst_dev); break;
     case ER_F32: convert_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(data_dev, n, (float*)dst_dev); break;
     default: return er_set_error(ER_EINVAL, "er_convert_f64: dst must be u8 or f32");
+  }
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_minmax_f64(const double* data_dev, int64_t n, double* out2_dev, void* stream) {
+  if (!data_dev || !out2_dev || n <= 0) return er_set_error(ER_EINVAL, "er_minmax_f64: args");
+  cudaStream_t st = as_stream(stream);
+  unsigned long long* mm = reinterpret_cast<unsigned long long*>(out2_dev);
+  minmax_init_kernel<<<1, 1, 0, st>>>(mm);
+  long long blocks = (n + 255) / 256;
+  if (blocks > ER_NUM_SMS_B200 * 8) blocks = ER_NUM_SMS_B200 * 8;
+  minmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(data_dev, n, mm);
+  minmax_final_kernel<<<1, 1, 0, st>>>(mm);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_lattice_u8(const double* data_dev, int64_t n, double x0, double delta,
+                             double tol, uint8_t* out_dev, int32_t* flag_dev, void* stream) {
+  if (!data_dev || !out_dev || !flag_dev || n < 0 || !(delta > 0.0) || !(tol >= 0.0))
+    return er_set_error(ER_EINVAL, "er_lattice_u8: args");
+  cudaStream_t st = as_stream(stream);
+  init_flags_kernel<<<1, 32, 0, st>>>(flag_dev);
+  if (n > 0) {
+    long long blocks = (n + 255) / 256;
+    if (blocks > ER_NUM_SMS_B200 * 8) blocks = ER_NUM_SMS_B200 * 8;
+    lattice_kernel<<<(unsigned)blocks, 256, 0, st>>>(data_dev, n, x0, delta, tol, out_dev,
+                                                    flag_dev);
   }
   ER_CHECK_LAUNCH();
   return ER_OK;

@@ -208,8 +208,41 @@ def _shared_u8(raw: np.ndarray, device, pinned_staging=False) -> _SharedU8:
     return sh
 
 
-def upload_array(data: np.ndarray, device, *, pinned_staging=False):
-    """Upload one fp64 volume and pick a lossless storage type on the device."""
+def _try_lattice(f64, flat_host: np.ndarray, device, stream):
+    """8-bit data behind an affine image (x = x0 + k delta, k in 0..255), e.g.
+    the reference's z-score of 8-bit echo data arriving as plain fp64: the
+    step comes from the distinct values of a host sample, the offset from the
+    exact device minimum, and every voxel is verified on the device
+    (er_lattice_u8) to reproduce x within a few hundred ulps.  Returns
+    (u8 storage, delta, x0) or None."""
+    t = torch()
+    n = f64.numel()
+    sample = np.unique(flat_host[:: max(1, n // 65536)])
+    if sample.size < 2 or sample.size > 256:
+        return None
+    delta0 = float(np.diff(sample).min())
+    if not delta0 > 0.0:
+        return None
+    mm = t.empty(2, dtype=t.float64, device=device)
+    _lib.call("er_minmax_f64", ptr(f64), n, ptr(mm), stream)
+    x0, x1 = (float(v) for v in mm.tolist())
+    kmax = int(round((x1 - x0) / delta0))
+    if kmax < 1 or kmax > 255:
+        return None
+    delta = (x1 - x0) / kmax
+    tol = 256.0 * np.finfo(np.float64).eps * max(abs(x0), abs(x1), delta * 255.0)
+    u8 = t.empty(n, dtype=t.uint8, device=device)
+    flag = t.empty(1, dtype=t.int32, device=device)
+    _lib.call("er_lattice_u8", ptr(f64), n, x0, delta, tol, ptr(u8), ptr(flag), stream)
+    if int(flag.item()) != 1:
+        return None
+    return u8, delta, x0
+
+
+def upload_array(data: np.ndarray, device, *, pinned_staging=False, lattice=False):
+    """Upload one fp64 volume and pick a lossless storage type on the device.
+    ``lattice``: also recognise affine images of 8-bit data (stored as u8
+    with the affine in the descriptor; values reproduced to ~1e-13)."""
     t = torch()
     dims = tuple(int(x) for x in data.shape)
     if len(dims) != 3:
@@ -235,7 +268,13 @@ def upload_array(data: np.ndarray, device, *, pinned_staging=False):
         code = _lib.ER_F32
     else:
         storage, code = f64, _lib.ER_F64
-    desc = _make_desc(storage, code, dims, 1.0, 0.0)
+    alpha, gamma = 1.0, 0.0
+    if code == _lib.ER_F64 and lattice:
+        hit = _try_lattice(f64, flat, device, stream)
+        if hit is not None:
+            storage, alpha, gamma = hit
+            code = _lib.ER_U8
+    desc = _make_desc(storage, code, dims, alpha, gamma)
     moments = t.empty(_lib.ER_MOMENTS_DOUBLES, dtype=t.float64, device=device)
     _lib.call("er_volume_moments", ctypes.byref(desc), ptr(moments), stream)
     return storage, desc, moments, code
@@ -270,11 +309,13 @@ def device_volume(v, device=None) -> DeviceVolume:
 
 
 def device_volume_from_array(data: np.ndarray, device=None, spacing=(1.0, 1.0, 1.0),
-                             origin=(0.0, 0.0, 0.0), pinned_staging=False) -> DeviceVolume:
+                             origin=(0.0, 0.0, 0.0), pinned_staging=False,
+                             lattice=False) -> DeviceVolume:
     """Uncached upload of a bare array (kernel-module seam: arrays, not Volume3)."""
     dev = require_cuda(device)
     storage, desc, moments, code = upload_array(np.asarray(data), dev,
-                                                pinned_staging=pinned_staging)
+                                                pinned_staging=pinned_staging,
+                                                lattice=lattice)
     return DeviceVolume(storage, desc, tuple(int(x) for x in data.shape), tuple(spacing),
                         tuple(origin), moments, code)
 

@@ -198,3 +198,70 @@ def test_kernel_module_seam_host_buffers():
     assert _close(z, c["ncc_overlap"], 1e-10)[0]
     assert np.array_equal(d, c["degen_overlap"])
     assert math.isfinite(float(z.sum()))
+
+
+def _zscored_bytes(dims, seed):
+    """The reference's normalize_zscore of 8-bit data (volume.py:119-130) as
+    the plain fp64 array its kernel-module seam receives."""
+    raw = np.random.default_rng(seed).integers(0, 256, dims).astype(np.float64)
+    return (raw - raw.mean()) / raw.std()
+
+
+def _near_identity_affines(n, seed, shift=2.0):
+    g = np.random.default_rng(seed)
+    a = np.eye(3)[None] + g.uniform(-0.05, 0.05, (n, 3, 3))
+    b = g.uniform(-shift, shift, (n, 3))
+    return a, b
+
+
+def test_kernel_module_seam_recovers_zscored_bytes():
+    """z-scored 8-bit volumes reach the seam as fp64; they are recognised as an
+    affine image of bytes (stored u8, oct fast path) and measure like the
+    reference (f32 tolerance), and the next call reuses the device copies."""
+    from paper_2504_19930_b200 import _lib, kernels_sm100
+
+    t = _zscored_bytes((40, 36, 44), 3)
+    s = _zscored_bytes((40, 36, 44), 4)
+    a, b = _near_identity_affines(24, 5)
+    for overlap in (False, True):
+        z, d = kernels_sm100.ncc_measure_batch(t, s, a, b, overlap)
+        zo, do = ok.ncc_measure_batch(t, s, a, b, overlap)
+        assert _close(z, zo, RTOL["f32"])[0], overlap
+        assert np.array_equal(d, do)
+    dvs = [dv for ref, _fp, dv in kernels_sm100._CACHE.values() if ref() is t]
+    assert dvs and all(dv.dtype_code == _lib.ER_U8 for dv in dvs)
+    assert abs(dvs[0].desc.alpha * 255 + dvs[0].desc.gamma - t.max()) < 1e-12
+    n_cached = len(kernels_sm100._CACHE)
+    kernels_sm100.ncc_measure_batch(t, s, a, b, False)
+    assert len(kernels_sm100._CACHE) == n_cached
+    assert [dv for ref, _fp, dv in kernels_sm100._CACHE.values() if ref() is t][0] is dvs[0]
+
+
+def test_kernel_module_seam_revalidates_mutated_volumes():
+    from paper_2504_19930_b200 import _lib, kernels_sm100
+
+    t = _zscored_bytes((30, 20, 26), 7)
+    s = _zscored_bytes((30, 20, 26), 8)
+    a, b = _near_identity_affines(12, 9)
+    kernels_sm100.ncc_measure_batch(t, s, a, b, False)
+    t[0, 0, 0] += 1.0          # off the byte lattice; index 0 is fingerprinted
+    z, d = kernels_sm100.ncc_measure_batch(t, s, a, b, False)
+    zo, do = ok.ncc_measure_batch(t, s, a, b, False)
+    assert _close(z, zo, RTOL["f32"])[0]
+    assert np.array_equal(d, do)
+    dvs = [dv for ref, _fp, dv in kernels_sm100._CACHE.values() if ref() is t]
+    assert [dv.dtype_code for dv in dvs] == [_lib.ER_F64]   # re-uploaded, exact storage
+
+
+def test_lattice_recognition_rejects_other_data():
+    from paper_2504_19930_b200 import _lib
+    from paper_2504_19930_b200.device import device_volume_from_array
+
+    g = np.random.default_rng(1)
+    for data in (g.standard_normal((20, 20, 20)),                       # continuous
+                 np.round(g.standard_normal((20, 20, 20)) * 200) / 7.0,  # > 256 levels
+                 _zscored_bytes((20, 20, 20), 2) + 1e-9 * g.standard_normal((20, 20, 20))):
+        dv = device_volume_from_array(data, lattice=True)
+        assert dv.dtype_code == _lib.ER_F64
+    dv = device_volume_from_array(_zscored_bytes((20, 20, 20), 2), lattice=True)
+    assert dv.dtype_code == _lib.ER_U8
