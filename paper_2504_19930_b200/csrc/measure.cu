@@ -96,6 +96,7 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 #define ER_OCT_FMUL2 1
 #endif
 
+
 // kernels_numba.py:88-113, bit-exact (IEEE division, ceil/floor, same guards)
 __device__ __forceinline__ void k_interval(double c0, double slope, double limit, int& klo,
                                            int& khi) {
