@@ -88,6 +88,9 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 #endif
 // fp32 paths: keep the per-lane fp64 group accumulators in shared memory
 // (touched once per row) instead of 6 registers of the voxel loop
+#ifndef ER_MIN_TILES
+#define ER_MIN_TILES 8
+#endif
 #ifndef ER_OCT_SMEM_ACC
 #define ER_OCT_SMEM_ACC 1
 #endif
@@ -824,7 +827,15 @@ Geom make_geom(const er_volume* t, const er_volume* s) {
   g.sx = s->nx;
   g.sy = s->ny;
   g.sz = s->nz;
-  int ppt = kRowsPerTile / (g.ny > 0 ? g.ny : 1);
+  // tile = whole target planes, at most kRowsPerTile rows; small volumes are
+  // cut into >= ER_MIN_TILES tiles (>= 256 rows each) so that few-particle
+  // launches still fill the GPU.  Depends on the dims only: a particle's
+  // partial sums never depend on P or on the GPU count.
+  const long long rows_all = (long long)g.nx * g.ny;
+  long long rows_tile = rows_all / ER_MIN_TILES;
+  if (rows_tile < 256) rows_tile = 256;
+  if (rows_tile > kRowsPerTile) rows_tile = kRowsPerTile;
+  int ppt = (int)(rows_tile / (g.ny > 0 ? g.ny : 1));
   if (ppt < 1) ppt = 1;
   if (ppt > g.nx) ppt = g.nx;
   g.planes_per_tile = ppt;

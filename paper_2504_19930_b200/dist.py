@@ -59,12 +59,12 @@ def plan(n: int) -> ShardPlan:
 
 def allgather_shards(local, plan: ShardPlan, out):
     """Gather every rank's padded shard of ``local`` (length plan.shard) into
-    ``out`` (length plan.shard * world) and return the first n entries."""
+    ``out`` (length plan.shard * world) and return the first n entries (on a
+    single rank: ``local`` itself, no copy)."""
     import torch.distributed as td
 
     if plan.world == 1:
-        out[: plan.count].copy_(local[: plan.count])
-        return out[: plan.n]
+        return local[: plan.n]   # the local shard is the whole set: no copy
     td.all_gather_into_tensor(out, local)
     return out[: plan.n]
 
