@@ -65,9 +65,6 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_FRAC_I2F
 #define ER_FRAC_I2F 1
 #endif
-#ifndef ER_OCT_TEX
-#define ER_OCT_TEX 0
-#endif
 #ifndef ER_OCT_TILE_MAJOR
 #define ER_OCT_TILE_MAJOR 1
 #endif
@@ -343,13 +340,6 @@ __device__ __forceinline__ float byte_magic(unsigned w, unsigned sel) {
   return __int_as_float(__byte_perm(w, 0x4B000000u, sel | 0x7650u));
 }
 
-// lerp between two bytes of a word: a + f (b - a) with (b - a) formed exactly
-// on the 2^23-offset floats (one FADD fewer than converting both bytes)
-__device__ __forceinline__ float lerp_bytes(unsigned w, unsigned sa, unsigned sb, float f) {
-  const float A = byte_magic(w, sa), B = byte_magic(w, sb);
-  return fmaf(f, B - A, A - 8388608.0f);
-}
-
 __device__ __forceinline__ double byte_f64(unsigned w, unsigned sel) {
   return __hiloint2double(0x43300000, __byte_perm(w, 0u, sel | 0x4440u)) - 4503599627370496.0;
 }
@@ -425,8 +415,7 @@ template <typename TT, int LERP, int BITS = 0>
 __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOCKS_F32 : 3)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
-                       const OctGeom og, Partial* __restrict__ part,
-                       cudaTextureObject_t otex) {
+                       const OctGeom og, Partial* __restrict__ part) {
   using F = Fix<LERP == ER_LERP_F32 ? 32 : 40>;
 #if ER_OCT_TILE_MAJOR
   // tile-major launch order: the CTAs resident at any moment work on the same
@@ -572,11 +561,7 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
           cw += kLanes * dw;
           continue;
         }
-#if ER_OCT_TEX
-        const uint2 c8 = tex1Dfetch<uint2>(otex, cell);
-#else
         const uint2 c8 = ld_oct(oct + (unsigned)er_idx(cell, ncells));
-#endif
         const float yf = ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
         if (LERP == ER_LERP_F32) {
 #if ER_OCT_FMUL2
@@ -739,29 +724,6 @@ __global__ void build_oct_kernel(const uint8_t* __restrict__ s, int sx, int sy, 
   }
 }
 
-#if ER_OCT_TEX
-// experiment: linear texture objects over oct buffers, cached per pointer
-cudaTextureObject_t oct_texture(const uint2* p, size_t cells) {
-  static const void* last_p = nullptr;
-  static size_t last_n = 0;
-  static cudaTextureObject_t last_t = 0;
-  if (p == last_p && cells == last_n) return last_t;
-  cudaResourceDesc rd = {};
-  rd.resType = cudaResourceTypeLinear;
-  rd.res.linear.devPtr = const_cast<uint2*>(p);
-  rd.res.linear.desc = cudaCreateChannelDesc<uint2>();
-  rd.res.linear.sizeInBytes = cells * sizeof(uint2);
-  cudaTextureDesc td = {};
-  td.readMode = cudaReadModeElementType;
-  td.filterMode = cudaFilterModePoint;
-  cudaTextureObject_t t = 0;
-  cudaCreateTextureObject(&t, &rd, &td, nullptr);
-  last_p = p;
-  last_n = cells;
-  last_t = t;
-  return t;
-}
-#endif
 
 struct Affines {
   double as, gs, at, gt;
@@ -925,12 +887,8 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
     const OctGeom og{src->ny + 1, src->nz + 1, (long long)P};
     const unsigned blocks = (unsigned)(P * g.ntiles);
     const uint2* lay = (const uint2*)(use_bits ? src->bitoct_dev : src->oct_dev);
-    cudaTextureObject_t otex = 0;
-#if ER_OCT_TEX
-    if (!use_bits) otex = oct_texture(lay, (size_t)(src->nx + 1) * (src->ny + 1) * (src->nz + 1));
-#endif
 #define ER_OCT(TT, L, B) \
-  measure_oct_kernel<TT, L, B><<<blocks, kOctThreads, 0, st>>>((const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part, otex)
+  measure_oct_kernel<TT, L, B><<<blocks, kOctThreads, 0, st>>>((const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part)
     const bool f32 = lerp_mode == ER_LERP_F32;
     if (use_bits) {
       switch (tgt->dtype) {
