@@ -215,7 +215,7 @@ def run_reference(args):
     ok.ncc_measure_batch(t.data, s.data, a[:p], b[:p], False, threads)
     one = time.perf_counter() - t0
     budget = 150.0 / max(1, args.steps + args.warmup)
-    p = max(threads, min(a.shape[0], int(p * budget / max(one, 1e-3))))
+    p = min(a.shape[0], max(threads, int(p * budget / max(one, 1e-3))))
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
