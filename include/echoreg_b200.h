@@ -39,6 +39,9 @@ extern "C" {
 #define ER_LERP_F32 0      /* fp32 lerps on fp64 coordinates/fractions      */
 #define ER_LERP_F64 1      /* fp64 lerps (FMA), fp64 everywhere             */
 #define ER_LERP_EXACT 2    /* fp64 lerps in the reference's a(1-f)+bf order */
+#define ER_LERP_NEAREST 3  /* nearest voxel, ties to the upper one: the north
+                              star's option for binary masks (opt-in; the
+                              reference itself samples masks trilinearly) */
 
 typedef struct er_volume {
   const void *data_dev; /* device pointer */

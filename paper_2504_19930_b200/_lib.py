@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "_lib", "libechoreg_sm100.so")
 
 ER_OK, ER_EINVAL, ER_ECUDA, ER_EWEIGHTS = 0, 1, 2, 3
 ER_U8, ER_F32, ER_F64 = 0, 1, 2
-ER_LERP_F32, ER_LERP_F64, ER_LERP_EXACT = 0, 1, 2
+ER_LERP_F32, ER_LERP_F64, ER_LERP_EXACT, ER_LERP_NEAREST = 0, 1, 2, 3
 ER_MOMENTS_DOUBLES = 1026
 ER_NCC_SUMS_DOUBLES = 1782
 ER_TRACE_STRIDE = 12

@@ -171,6 +171,10 @@ __device__ __forceinline__ double sample(const ST* __restrict__ src, double u, d
   const int o11 = (i1 * g.sy + j1) * g.sz;
   const long long ns = (long long)g.sx * g.sy * g.sz;  // er_idx extent (debug builds)
   (void)ns;
+  if (LERP == ER_LERP_NEAREST) {  // fraction >= 0.5 -> upper corner
+    const int o = fv >= 0.5 ? (fu >= 0.5 ? o11 : o01) : (fu >= 0.5 ? o10 : o00);
+    return ldd(src, er_idx(o + (fw >= 0.5 ? k1 : k0), ns));
+  }
   if (LERP == ER_LERP_F32) {
     const float x000 = ldf(src, er_idx(o00 + k0, ns)), x100 = ldf(src, er_idx(o10 + k0, ns));
     const float x010 = ldf(src, er_idx(o01 + k0, ns)), x110 = ldf(src, er_idx(o11 + k0, ns));
@@ -412,11 +416,13 @@ struct OctGeom {
 // BITS = 1: `oct` points at the bit-oct layout of a binary source (1 byte per
 // cell) and the lerps run in fp32 (row partials folded per row as below).
 template <typename TT, int LERP, int BITS = 0>
-__global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINBLOCKS_F32 : 3)
+__global__ void __launch_bounds__(kOctThreads, LERP != ER_LERP_F64 ? ER_OCT_MINBLOCKS_F32 : 3)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
                        const OctGeom og, Partial* __restrict__ part) {
-  using F = Fix<LERP == ER_LERP_F32 ? 32 : 40>;
+  // fp32-class modes (fp32 lerps, nearest) use Q32.32 coordinates and fp32 row partials
+  constexpr bool kF32 = LERP != ER_LERP_F64;
+  using F = Fix<kF32 ? 32 : 40>;
 #if ER_OCT_TILE_MAJOR
   // tile-major launch order: the CTAs resident at any moment work on the same
   // target slab for many particles, so the union of their source footprints
@@ -487,12 +493,12 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
     TgtAcc<TT> ty;
     float px = 0.f, pxx = 0.f, pyx = 0.f;
     double qx = 0.0, qxx = 0.0, qyx = 0.0;
-    constexpr bool kSmemAcc = ER_OCT_SMEM_ACC && (LERP == ER_LERP_F32 || BITS);
+    constexpr bool kSmemAcc = ER_OCT_SMEM_ACC && (kF32 || BITS);
     if (kSmemAcc) racc[threadIdx.x] = make_double3(0.0, 0.0, 0.0);
     // row start in fixed point (per lane: its own row)
     // (the +1.0 voxel shift to the padded cell index is an exact integer add,
     // so the cell index below is a plain non-negative 32-bit IMAD chain)
-    const long long one = 1LL << (LERP == ER_LERP_F32 ? 32 : 40);
+    const long long one = 1LL << (kF32 ? 32 : 40);
     // the lane's row record goes to shared memory (broadcast reads below), so
     // it does not occupy registers across the voxel loop
     RowRec& mine = rrec[warp][lane];
@@ -540,7 +546,13 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
                                    (unsigned)er_idx(cell, ncells));
           const float yf = ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
           float x = (c == 0xFFu) ? 1.0f : 0.0f;
-          if (c != 0u && c != 0xFFu) {
+          if (LERP == ER_LERP_NEAREST) {
+            // corner bit: u -> bit 0, v -> bit 1, w -> bit 2 (bit b = byte b of
+            // the oct word); fraction >= 0.5 <=> bit 31 of the fixed-point word
+            const unsigned b = ((unsigned)cu >> 31) | (((unsigned)cv >> 31) << 1) |
+                               (((unsigned)cw >> 31) << 2);
+            x = (float)((c >> b) & 1u);
+          } else if (c != 0u && c != 0xFFu) {
             const float fu = F::frac32(cu), fv = F::frac32(cv), fw = F::frac32(cw);
             auto bit = [c](int b) { return ((c >> b) & 1u) ? 1.0f : 0.0f; };
             const float2 P0 = make_float2(bit(0), bit(4)), P1 = make_float2(bit(1), bit(5));
@@ -563,7 +575,17 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
         }
         const uint2 c8 = ld_oct(oct + (unsigned)er_idx(cell, ncells));
         const float yf = ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
-        if (LERP == ER_LERP_F32) {
+        if (LERP == ER_LERP_NEAREST) {
+          // nearest corner byte: u -> byte bit 0, v -> byte bit 1, w -> word
+          const unsigned sel = ((unsigned)cu >> 31) | (((unsigned)cv >> 31) << 1);
+          const unsigned wd = ((unsigned)cw >> 31) ? c8.y : c8.x;
+          const float x = (float)__byte_perm(wd, 0u, 0x4440u | sel);
+          const float2 acc = __ffma2_rn(make_float2(x, x), make_float2(1.0f, x),
+                                        make_float2(px, pxx));
+          px = acc.x;
+          pxx = acc.y;
+          pyx = fmaf(yf, x, pyx);
+        } else if (LERP == ER_LERP_F32) {
 #if ER_OCT_FMUL2
           const float2 fuv = __fmul2_rn(make_float2(__uint2float_rz((unsigned)cu),
                                                     __uint2float_rz((unsigned)cv)),
@@ -616,7 +638,7 @@ __global__ void __launch_bounds__(kOctThreads, LERP == ER_LERP_F32 ? ER_OCT_MINB
         cv += kLanes * dv;
         cw += kLanes * dw;
       }
-      if (LERP == ER_LERP_F32 || BITS) {  // fp32 row partials (<= nz/kLanes voxels) -> fp64
+      if (kF32 || BITS) {  // fp32 row partials (<= nz/kLanes voxels) -> fp64
         if (kSmemAcc) {
           double3 a = racc[threadIdx.x];
           a.x += (double)px;
@@ -826,6 +848,7 @@ void launch_lerp(int lerp, const er_volume* t, const er_volume* s, const double*
   switch (lerp) {
     case ER_LERP_F32: launch_typed<TT, ST, ER_LERP_F32>(t, s, A, B, g, part, P, st); break;
     case ER_LERP_F64: launch_typed<TT, ST, ER_LERP_F64>(t, s, A, B, g, part, P, st); break;
+    case ER_LERP_NEAREST: launch_typed<TT, ST, ER_LERP_NEAREST>(t, s, A, B, g, part, P, st); break;
     default: launch_typed<TT, ST, ER_LERP_EXACT>(t, s, A, B, g, part, P, st); break;
   }
 }
@@ -868,7 +891,7 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
   if (P == 0) return ER_OK;
   if (!A_dev || !b_dev || !ncc_dev || !degen_dev || !tgt_moments_dev)
     return er_set_error(ER_EINVAL, "er_measure_ncc: null pointer");
-  if (lerp_mode < ER_LERP_F32 || lerp_mode > ER_LERP_EXACT)
+  if (lerp_mode < ER_LERP_F32 || lerp_mode > ER_LERP_NEAREST)
     return er_set_error(ER_EINVAL, "er_measure_ncc: bad lerp_mode");
   const Geom g = make_geom(tgt, src);
   const size_t need = (size_t)P * (size_t)g.ntiles * sizeof(Partial);
@@ -881,7 +904,8 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
   // (the oct kernel's per-tile group slots assume a tile of <= kRowsPerTile rows)
   // (the oct kernels' per-tile group slots assume a tile of <= kRowsPerTile rows)
   const bool fast = lerp_mode != ER_LERP_EXACT && tgt->ny <= kRowsPerTile && src->dtype == ER_U8;
-  const bool use_bits = fast && lerp_mode == ER_LERP_F32 && src->bitoct_dev;
+  const bool use_bits =
+      fast && (lerp_mode == ER_LERP_F32 || lerp_mode == ER_LERP_NEAREST) && src->bitoct_dev;
   const bool use_oct = fast && !use_bits && src->oct_dev;
   if (use_bits || use_oct) {
     const OctGeom og{src->ny + 1, src->nz + 1, (long long)P};
@@ -889,20 +913,32 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
     const uint2* lay = (const uint2*)(use_bits ? src->bitoct_dev : src->oct_dev);
 #define ER_OCT(TT, L, B) \
   measure_oct_kernel<TT, L, B><<<blocks, kOctThreads, 0, st>>>((const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part)
-    const bool f32 = lerp_mode == ER_LERP_F32;
+#define ER_OCT_BITS(TT)                                                   \
+  do {                                                                    \
+    if (lerp_mode == ER_LERP_NEAREST) ER_OCT(TT, ER_LERP_NEAREST, 1);     \
+    else ER_OCT(TT, ER_LERP_F32, 1);                                      \
+  } while (0)
+#define ER_OCT_BYTES(TT)                                                  \
+  do {                                                                    \
+    if (lerp_mode == ER_LERP_NEAREST) ER_OCT(TT, ER_LERP_NEAREST, 0);     \
+    else if (lerp_mode == ER_LERP_F32) ER_OCT(TT, ER_LERP_F32, 0);        \
+    else ER_OCT(TT, ER_LERP_F64, 0);                                      \
+  } while (0)
     if (use_bits) {
       switch (tgt->dtype) {
-        case ER_U8: ER_OCT(uint8_t, ER_LERP_F32, 1); break;
-        case ER_F32: ER_OCT(float, ER_LERP_F32, 1); break;
-        default: ER_OCT(double, ER_LERP_F32, 1); break;
+        case ER_U8: ER_OCT_BITS(uint8_t); break;
+        case ER_F32: ER_OCT_BITS(float); break;
+        default: ER_OCT_BITS(double); break;
       }
     } else {
       switch (tgt->dtype) {
-        case ER_U8: if (f32) ER_OCT(uint8_t, ER_LERP_F32, 0); else ER_OCT(uint8_t, ER_LERP_F64, 0); break;
-        case ER_F32: if (f32) ER_OCT(float, ER_LERP_F32, 0); else ER_OCT(float, ER_LERP_F64, 0); break;
-        default: if (f32) ER_OCT(double, ER_LERP_F32, 0); else ER_OCT(double, ER_LERP_F64, 0); break;
+        case ER_U8: ER_OCT_BYTES(uint8_t); break;
+        case ER_F32: ER_OCT_BYTES(float); break;
+        default: ER_OCT_BYTES(double); break;
       }
     }
+#undef ER_OCT_BITS
+#undef ER_OCT_BYTES
 #undef ER_OCT
   } else {
     switch (tgt->dtype) {

@@ -15,7 +15,8 @@ from .device import (WORKSPACE, DeviceVolume, device_volume, ptr, require_cuda,
                      stream_ptr, torch)
 from .errors import BadConfig
 
-LERP_MODES = {"f32": _lib.ER_LERP_F32, "f64": _lib.ER_LERP_F64, "exact": _lib.ER_LERP_EXACT}
+LERP_MODES = {"f32": _lib.ER_LERP_F32, "f64": _lib.ER_LERP_F64, "exact": _lib.ER_LERP_EXACT,
+              "nearest": _lib.ER_LERP_NEAREST}
 
 
 def lerp_code(precision: str) -> int:
@@ -38,7 +39,7 @@ def measure(tdv: DeviceVolume, sdv: DeviceVolume, A, B, overlap: bool, precision
     ncc, degen, n_in = out
     if P == 0:
         return ncc, degen, n_in
-    if precision == "f32":
+    if precision in ("f32", "nearest"):
         sdv.ensure_fast_layout()       # bit-oct for binary sources, else oct
     elif precision == "f64":
         sdv.ensure_oct()

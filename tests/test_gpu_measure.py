@@ -265,3 +265,71 @@ def test_lattice_recognition_rejects_other_data():
         assert dv.dtype_code == _lib.ER_F64
     dv = device_volume_from_array(_zscored_bytes((20, 20, 20), 2), lattice=True)
     assert dv.dtype_code == _lib.ER_U8
+
+
+def _nearest_ncc_numpy(tgt, src, a, b, overlap):
+    """Test-only: the reference _ncc_kernel (kernels_numba.py:116-189) with the
+    trilinear sample replaced by the nearest corner of the same clamped cell
+    (fraction >= 0.5 -> upper) -- the opt-in ER_LERP_NEAREST semantics."""
+    nx, ny, nz = tgt.shape
+    sx, sy, sz = src.shape
+    i, j, k = np.meshgrid(np.arange(nx, dtype=np.float64), np.arange(ny, dtype=np.float64),
+                          np.arange(nz, dtype=np.float64), indexing="ij")
+    out = np.zeros(a.shape[0])
+    for p in range(a.shape[0]):
+        A, B = a[p], b[p]
+        u = (A[0, 0] * i + A[0, 1] * j + B[0]) + A[0, 2] * k
+        v = (A[1, 0] * i + A[1, 1] * j + B[1]) + A[1, 2] * k
+        w = (A[2, 0] * i + A[2, 1] * j + B[2]) + A[2, 2] * k
+        inb = (u >= 0) & (u <= sx - 1) & (v >= 0) & (v <= sy - 1) & (w >= 0) & (w <= sz - 1)
+
+        def near(c, n):
+            c0 = np.clip(np.floor(c), 0, None).astype(np.int64)
+            c1 = c0 + 1
+            over = c1 > n - 1
+            c1 = np.where(over, n - 1, c1)
+            c0 = np.where(over, np.maximum(c1 - 1, 0), c0)
+            return np.where(c - c0 >= 0.5, c1, c0)
+
+        x = np.zeros_like(u)
+        x[inb] = src[near(u[inb], sx), near(v[inb], sy), near(w[inb], sz)]
+        t = tgt
+        if overlap:
+            t, x = t[inb], x[inb]
+        n = t.size
+        st, ss = t.sum(), x.sum()
+        sst = (t * t).sum() - st * st / n
+        sss = (x * x).sum() - ss * ss / n
+        sts = (t * x).sum() - st * ss / n
+        out[p] = 0.0 if sst / n < 1e-12 or sss / n < 1e-12 else sts * sts / (sst * sss)
+    return out
+
+
+@pytest.mark.parametrize("kind", ["mask", "u8", "f64"])
+@pytest.mark.parametrize("overlap", [False, True])
+def test_nearest_sampling_opt_in(kind, overlap):
+    """Executor(precision="nearest"): the north star's nearest-neighbour
+    sampling (opt-in; the reference samples trilinearly) on the bit-oct mask
+    path, the 8-bit oct path and the generic fp64-storage path."""
+    from paper_2504_19930_b200 import Executor, Volume3
+    from paper_2504_19930_b200.device import device_volume
+
+    g = np.random.default_rng(11)
+    dims = (22, 19, 26)
+    if kind == "mask":
+        tgt = (g.random(dims) > 0.6).astype(np.float64)
+        src = (g.random(dims) > 0.5).astype(np.float64)
+    elif kind == "u8":
+        tgt = g.integers(0, 256, dims).astype(np.float64)
+        src = g.integers(0, 256, dims).astype(np.float64)
+    else:
+        tgt, src = g.standard_normal(dims), g.standard_normal(dims)
+    a, b = _near_identity_affines(16, 12, shift=3.0)
+    mats = np.zeros((16, 4, 4))
+    mats[:, :3, :3], mats[:, :3, 3], mats[:, 3, 3] = a, b, 1.0   # unit grids: index affine = matrix
+    tv, sv = Volume3(tgt), Volume3(src)
+    z, d = Executor(precision="nearest").measure_ncc(tv, sv, mats, overlap)
+    want = _nearest_ncc_numpy(tgt, src, a, b, overlap)
+    assert _close(z, want, 1e-4)[0], (kind, z[:4], want[:4])
+    expect_code = {"mask": 0, "u8": 0, "f64": 2}[kind]
+    assert device_volume(sv).dtype_code == expect_code

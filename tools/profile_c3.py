@@ -2,7 +2,7 @@ import cProfile, os, pstats, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2504_19930_b200 import Executor, SmcConfig, register_sequence, Sequence4
-from paper_2504_19930_b200.phantom import echo_case
+from paper_2504_19930_b200.phantom_device import echo_case_device as echo_case
 case = echo_case(frames=30, seed=0)
 register_sequence(Sequence4(case.target.frames[:2]), Sequence4(case.source.frames[:2]),
                   case.target_masks[:2], case.source_masks[:2],
