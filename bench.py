@@ -184,7 +184,7 @@ def cpu_reference_rate(t, s, a, b, seconds, threads=0):
 def first_iteration_affines(t, s, n, seed=0):
     """Host copy of the particle set of SMC iteration 0 (init + predict, seed 0)."""
     from paper_2504_19930_b200 import SmcConfig
-    from paper_2504_19930_b200.smc import ParticleSet, init_particles, predict
+    from paper_2504_19930_b200.smc import init_particles, predict
     from paper_2504_19930_b200.geometry import index_affine_batch, to_matrix, RigidParams
 
     cfg = SmcConfig(n_particles=n, seed=seed)

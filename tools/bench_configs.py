@@ -129,7 +129,7 @@ def c4():
 
 
 def c5(pmax=262144):
-    from paper_2504_19930_b200 import SmcConfig, Volume3, normalize_zscore, ops
+    from paper_2504_19930_b200 import SmcConfig, normalize_zscore
     from paper_2504_19930_b200 import smc as dsmc
     from paper_2504_19930_b200.backend import Executor
     from paper_2504_19930_b200.phantom_device import echo_case_device

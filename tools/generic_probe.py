@@ -1,6 +1,6 @@
 """Throughput of the generic measurement path (non-8-bit data): fp64 and
 fp32-representable volumes on the C2 grid, each precision mode."""
-import json, os, sys
+import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2504_19930_b200 import SmcConfig, Volume3, normalize_zscore, ops

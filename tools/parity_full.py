@@ -2,7 +2,7 @@
 iterations, 176x176x208 u8 echo pair, image mode): the device path against
 the reference algorithm (oracle/smc.py driving the bit-exact C kernel, all
 host threads).  Prints one JSON line."""
-import json, math, os, sys, time
+import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import bench

@@ -2,7 +2,6 @@
 (one tool per run): generic measurement (f32/f64 storage, 3 precisions),
 oct (u8) and bit-oct (binary) fast paths in full and overlap mode, odd
 shapes, predict/update, exhaustive grid, warps, Dice, NCC, histogram."""
-import math
 import os
 import sys
 

@@ -5,7 +5,7 @@ algorithm's final transform to ~1e-14 (tools/parity_full.py, tests), so it
 stands in for the reference here: for seeds 0..N-1 run C2 (image, 2000 x 50)
 and a C3-style mask registration (2000 x 50 on the 176x176x208 masks) in
 f32 / f64 / exact and report the final-transform differences."""
-import json, math, os, sys, time
+import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import bench
