@@ -161,6 +161,33 @@ __device__ double block_sum(double v, double* sh) {
   return sh[32];
 }
 
+// N independent fixed-order block sums in one pass (each value is reduced in
+// exactly the order block_sum uses, so the results are bit-identical to N
+// separate calls); sh must hold 33 * N doubles
+template <int N>
+__device__ void block_sum_n(double (&v)[N], double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < N; ++c) v[c] = warp_sum(v[c]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) sh[32 * c + warp] = v[c];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double t = lane < (kUpdThreads / 32) ? sh[32 * c + lane] : 0.0;
+      t = warp_sum(t);
+      if (lane == 0) sh[32 * N + c] = t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < N; ++c) v[c] = sh[32 * N + c];
+}
+
 // first-max argmax (np.argmax): larger value wins, ties -> lower index
 __device__ __forceinline__ void better(double& bv, long long& bi, double v, long long i) {
   if (v > bv || (v == bv && i < bi)) {
@@ -235,10 +262,15 @@ __global__ void __launch_bounds__(kUpdThreads)
                       double* __restrict__ cw, long long n, double beta, double ess_frac,
                       uint64_t seed, long long k, int est_best, er_smc_ctl* __restrict__ ctl,
                       double* __restrict__ trace) {
-  __shared__ double sh[40];
+  __shared__ double sh[33 * 7];
   __shared__ double shv[40];
   __shared__ long long shi[40];
   __shared__ int fire_sh;
+  // the resampling CDF lives in shared memory when it fits (binary searches
+  // then stay on-chip), else in the caller's scratch
+  constexpr int kCdfShared = 4096;
+  __shared__ double cw_sh[kCdfShared];
+  double* cdf = n <= kCdfShared ? cw_sh : cw;
   const int tid = threadIdx.x;
   const long long chunk = (n + kUpdThreads - 1) / kUpdThreads;
   const long long lo = min(n, tid * chunk), hi = min(n, lo + chunk);
@@ -252,7 +284,6 @@ __global__ void __launch_bounds__(kUpdThreads)
     ndeg += degen ? (double)degen[i] : 0.0;
   }
   block_argmax(bv, bi, shv, shi);
-  ndeg = block_sum(ndeg, sh);
   if (tid == 0 && bv > ctl->best_measurement) {
     ctl->best_measurement = bv;
     ctl->has_best = 1;
@@ -276,8 +307,10 @@ __global__ void __launch_bounds__(kUpdThreads)
     part2 = fma(wi, wi, part2);
     psum += wi;
   }
-  const double wsum = block_sum(psum, sh);
-  const double w2 = block_sum(part2, sh);
+  double r3[3] = {psum, part2, ndeg};
+  block_sum_n(r3, sh);
+  const double wsum = r3[0], w2 = r3[1];
+  ndeg = r3[2];
   const double ess = rn_div(1.0, w2);  // smc.py:227-229
   if (tid == 0) {
     if (fabs(wsum - 1.0) > 1e-9) ctl->error = ER_EWEIGHTS;  // smc.py:139-142
@@ -298,7 +331,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     double acc = block_exclusive_scan(run, sh);
     for (long long i = lo; i < hi; ++i) {
       acc += w[i];
-      cw[i] = acc;
+      cdf[i] = acc;
     }
     __syncthreads();
     __threadfence_block();
@@ -308,7 +341,7 @@ __global__ void __launch_bounds__(kUpdThreads)
       long long a = 0, b = n;
       while (a < b) {
         const long long mid = (a + b) >> 1;
-        if (cw[mid] <= pos) a = mid + 1;
+        if (cdf[mid] <= pos) a = mid + 1;
         else b = mid;
       }
       const long long idx = a < n - 1 ? a : n - 1;
@@ -328,11 +361,11 @@ __global__ void __launch_bounds__(kUpdThreads)
   __syncthreads();
 
   // estimate (smc.py:251-259) and trace row (smc.py:358-364)
-  double est[6];
+  double est[7];  // 6 weighted-mean components + sum of z (trace mean)
   for (int d = 0; d < 6; ++d) {
     double e = 0.0;
     for (long long i = lo; i < hi; ++i) e = fma(w[i], st_out[6 * i + d], e);
-    est[d] = block_sum(e, sh);
+    est[d] = e;
   }
   double zs = 0.0, zmax = -INFINITY;
   long long zi = 0;
@@ -340,7 +373,9 @@ __global__ void __launch_bounds__(kUpdThreads)
     zs += z_out[i];
     better(zmax, zi, z_out[i], i);
   }
-  const double zsum = block_sum(zs, sh);
+  est[6] = zs;
+  block_sum_n(est, sh);
+  const double zsum = est[6];
   block_argmax(zmax, zi, shv, shi);
   if (tid == 0) {
     const bool use_best = est_best && ctl->has_best;
