@@ -51,10 +51,12 @@ class Executor:
 
     workers: int = 1
     backend: str | None = None
-    # interpolation arithmetic: f32 (default; fp64 row starts + exact intervals,
-    # fixed-point coordinates, fp32 lerps) | f64 | exact (reference op order).
-    # All three reproduce the reference's final transforms to ~1e-14 on the
-    # seed sweeps of tests/test_gpu_seed_sweep.py.
+    # sampling arithmetic: f32 (default; fp64 row starts + exact intervals,
+    # fixed-point coordinates, fp32 lerps) | f64 | exact (reference op order)
+    # | nearest (opt-in nearest neighbour, not the reference's semantics).
+    # f64 / exact track the reference's final transforms to <= 5e-12 deg at
+    # full scale; f32 to 1e-14 on the small seed sweeps and within 0.03 deg at
+    # full scale.
     precision: str = "f32"
     device: int | None = None
 
