@@ -196,3 +196,47 @@ def test_recovers_the_reference_small_case():
     assert np.all(np.degrees(err[:3]) <= 6.0) and np.all(err[3:] <= 0.5)
     assert float(dice_under_transform(sm, tm, to_matrix(est, tm.physical_center()))) >= 0.94
     assert trace.ess[0] >= 1.0
+
+
+# ---- resampling and the fused measurement (E/geometry.py:188-200,
+#      E/kernels_numba.py:116-189; T/test_geometry.py, T/test_kernels.py) ----
+
+def test_resample_identity_integer_shift_and_trilinear_fields():
+    from paper_2504_19930_b200 import RigidParams, resample, to_matrix
+
+    g = np.random.default_rng(6)
+    src = g.standard_normal((9, 8, 10))
+    v = _vol(src)
+    assert np.array_equal(resample(v, v, np.eye(4)).data, src)
+    # integer translation == array shift with fill 0 (pull-back: out(x) = src(x + d))
+    moved = resample(v, v, to_matrix(RigidParams(tx=2.0, ty=-1.0, tz=0.0))).data
+    want = np.zeros_like(src)
+    want[:-2, 1:, :] = src[2:, :-1, :]
+    assert np.array_equal(moved, want)
+    # a trilinear polynomial field is reproduced exactly (up to rounding) anywhere
+    i, j, k = np.meshgrid(np.arange(9.0), np.arange(8.0), np.arange(10.0), indexing="ij")
+    c = g.uniform(-1, 1, 8)
+    f = lambda x, y, z: (c[0] + c[1] * x + c[2] * y + c[3] * z + c[4] * x * y + c[5] * x * z
+                         + c[6] * y * z + c[7] * x * y * z)
+    m = to_matrix(RigidParams(0.03, -0.02, 0.05, 0.3, -0.4, 0.2), v.physical_center())
+    out = resample(_vol(f(i, j, k)), v, m).data
+    pts = np.einsum("ab,bijk->aijk", m[:3, :3], np.stack([i, j, k])) + m[:3, 3][:, None, None, None]
+    inside = np.all((pts >= 0) & (pts <= np.array([8, 7, 9])[:, None, None, None]), axis=0)
+    assert inside.sum() > 300
+    assert np.allclose(out[inside], f(*pts)[inside], rtol=0, atol=1e-12)
+    assert np.all(out[~inside] == 0.0)
+
+
+@pytest.mark.parametrize("precision,tol", [("exact", 1e-9), ("f64", 1e-9), ("f32", 1e-4)])
+def test_fused_measurement_equals_composed_warp_then_ncc(precision, tol):
+    from paper_2504_19930_b200 import Executor, RigidParams, ncc, resample, to_matrix
+
+    g = np.random.default_rng(7)
+    t = _vol(g.integers(0, 256, (14, 12, 16)).astype(np.float64))
+    s = _vol(np.roll(t.data, 1, axis=0) + g.integers(0, 40, (14, 12, 16)))
+    mats = [to_matrix(RigidParams(*g.uniform(-0.1, 0.1, 3), *g.uniform(-2, 2, 3)),
+                      t.physical_center()) for _ in range(6)]
+    z, _ = Executor(precision=precision).measure_ncc(t, s, np.stack(mats))
+    for p, m in enumerate(mats):
+        want = float(ncc(t, resample(s, t, m)))
+        assert abs(z[p] - want) <= tol * max(want, 1e-12), (p, z[p], want)
