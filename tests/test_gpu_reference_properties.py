@@ -240,3 +240,70 @@ def test_fused_measurement_equals_composed_warp_then_ncc(precision, tol):
     for p, m in enumerate(mats):
         want = float(ncc(t, resample(s, t, m)))
         assert abs(z[p] - want) <= tol * max(want, 1e-12), (p, z[p], want)
+
+
+# ---- 4D pipeline, exhaustive search, phantom (T/test_pipeline.py,
+#      T/test_exhaustive.py, T/test_phantom.py) -------------------------------
+
+def _cycle(frames=3, amplitude=0.25, seed=3):
+    from paper_2504_19930_b200 import PhantomSpec, RigidParams, make_pair
+    from paper_2504_19930_b200.phantom_device import make_phantom_device
+
+    spec = PhantomSpec(dims=(24, 24, 24), frames=frames, outer_semiaxes=(9.0, 7.5, 10.0),
+                       inner_semiaxes=(6.0, 4.5, 7.0), amplitude=amplitude, seed=seed)
+    seq, masks = make_phantom_device(spec)
+    truth = RigidParams(math.radians(3.0), 0.0, math.radians(-2.0), 1.5, -1.0, 0.5)
+    return make_pair(seq, masks, truth)
+
+
+def test_pipeline_reports_errors_and_aggregates():
+    from paper_2504_19930_b200 import (Executor, Sequence4, SmcConfig, Volume3,
+                                       register_sequence)
+    from paper_2504_19930_b200.errors import GeometryMismatch, MissingMasks
+
+    case = _cycle()
+    cfg = SmcConfig(mode="mask", n_particles=64, n_iterations=4, seed=1)
+    rep = register_sequence(case.target, case.source, case.target_masks, case.source_masks,
+                            cfg, Executor(workers=2))
+    agg = rep.aggregates
+    assert abs(agg["ncc_after_mean"] - float(np.mean(rep.ncc_after))) <= 1e-12
+    assert abs(agg["dsc_before_std"] - float(np.std(rep.dsc_before))) <= 1e-12
+    assert len(rep.dsc_after) == len(rep.ncc_before) == 3
+    img = register_sequence(case.target, case.source, None, None,
+                            SmcConfig(n_particles=32, n_iterations=3, seed=1))
+    assert all(d is None for d in img.dsc_before + img.dsc_after)
+    with pytest.raises(MissingMasks):
+        register_sequence(case.target, case.source, None, None, cfg)
+    other = Sequence4([Volume3(f.data, (1.0, 1.0, 1.1)) for f in case.source.frames])
+    with pytest.raises(GeometryMismatch):
+        register_sequence(case.target, other, case.target_masks, case.source_masks, cfg)
+
+
+def test_exhaustive_identity_wins_when_aligned_and_beats_identity_score():
+    from paper_2504_19930_b200 import Executor, GridSpec, RigidParams, register_exhaustive
+
+    case = _cycle(frames=1)
+    tm, sm = case.target_masks[0], case.source_masks[0]
+    g = GridSpec(half_counts=(1, 0, 1, 1, 1, 0), step_r=3.0, step_t=1.5)
+    best, _ = register_exhaustive(tm, tm, g)
+    assert np.array_equal(best.to_array(), RigidParams().to_array())
+    best, value = register_exhaustive(tm, sm, g)
+    ident, _ = Executor().measure_ncc(tm, sm, np.eye(4))
+    assert float(value) >= float(ident[0])
+
+
+def test_device_phantom_cycle_properties():
+    from paper_2504_19930_b200 import PhantomSpec
+    from paper_2504_19930_b200.phantom_device import make_phantom_device
+
+    spec = PhantomSpec(dims=(24, 24, 24), frames=4, outer_semiaxes=(9.0, 7.5, 10.0),
+                       inner_semiaxes=(6.0, 4.5, 7.0), amplitude=0.3, seed=1)
+    seq, masks = make_phantom_device(spec)
+    assert seq.ed_index == 0
+    raw = [m.codec.raw for m in masks]
+    assert all(set(np.unique(r)) <= {0, 1} for r in raw)
+    assert np.all(raw[0] >= raw[2]) and raw[0].sum() > raw[2].sum()   # ED contains mid-cycle
+    frozen, _ = make_phantom_device(PhantomSpec(dims=(16, 16, 16), frames=3, amplitude=0.0,
+                                                outer_semiaxes=(6.0, 5.0, 7.0),
+                                                inner_semiaxes=(4.0, 3.0, 5.0), seed=4))
+    assert all(np.array_equal(f.data, frozen.frames[0].data) for f in frozen.frames)
