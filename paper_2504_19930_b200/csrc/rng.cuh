@@ -23,24 +23,43 @@
 #define ER_HD inline
 #endif
 
+// Device copies of the tables.  The ziggurat indexes them with a random byte
+// per lane, so __constant__ storage (broadcast cache) would serialise a warp's
+// divergent lookups; ER_ZIG_GLOBAL = 1 keeps them in global memory read
+// through the read-only L1 path instead.  (Each translation unit that
+// includes this header gets its own copy.)
+#ifndef ER_ZIG_GLOBAL
+#define ER_ZIG_GLOBAL 1
+#endif
 #if defined(__CUDACC__)
-// one translation unit (smc.cu) includes this header
+#if ER_ZIG_GLOBAL
+__device__ const uint64_t er_ki_double[256] = ER_KI_INIT;
+__device__ const double er_wi_double[256] = ER_WI_INIT;
+__device__ const double er_fi_double[256] = ER_FI_INIT;
+#else
 __constant__ uint64_t er_ki_double[256] = ER_KI_INIT;
 __constant__ double er_wi_double[256] = ER_WI_INIT;
 __constant__ double er_fi_double[256] = ER_FI_INIT;
+#endif
 #endif
 static const uint64_t er_host_ki_double[256] = ER_KI_INIT;
 static const double er_host_wi_double[256] = ER_WI_INIT;
 static const double er_host_fi_double[256] = ER_FI_INIT;
 
 #ifdef __CUDA_ARCH__
-#define ER_KI er_ki_double
-#define ER_WI er_wi_double
-#define ER_FI er_fi_double
+#if ER_ZIG_GLOBAL
+#define ER_KI_AT(i) __ldg(&er_ki_double[(i)])
+#define ER_WI_AT(i) __ldg(&er_wi_double[(i)])
+#define ER_FI_AT(i) __ldg(&er_fi_double[(i)])
 #else
-#define ER_KI er_host_ki_double
-#define ER_WI er_host_wi_double
-#define ER_FI er_host_fi_double
+#define ER_KI_AT(i) er_ki_double[(i)]
+#define ER_WI_AT(i) er_wi_double[(i)]
+#define ER_FI_AT(i) er_fi_double[(i)]
+#endif
+#else
+#define ER_KI_AT(i) er_host_ki_double[(i)]
+#define ER_WI_AT(i) er_host_wi_double[(i)]
+#define ER_FI_AT(i) er_host_fi_double[(i)]
 #endif
 
 struct ErPhilox {
@@ -273,9 +292,9 @@ ER_HD double er_standard_normal_from(Words& s) {
     r >>= 8;
     int sign = (int)(r & 0x1);
     uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-    double x = ER_MUL((double)rabs, ER_WI[idx]);
+    double x = ER_MUL((double)rabs, ER_WI_AT(idx));
     if (sign) x = -x;
-    if (rabs < ER_KI[idx]) return x;
+    if (rabs < ER_KI_AT(idx)) return x;
     if (idx == 0) {
       for (;;) {
         double xx = ER_MUL(-zinv, er_log1p(-er_u64_to_double(s.next())));
@@ -285,8 +304,9 @@ ER_HD double er_standard_normal_from(Words& s) {
           return ((rabs >> 8) & 0x1) ? -ER_ADD(zr, xx) : ER_ADD(zr, xx);
       }
     } else {
-      double f = ER_ADD(ER_MUL(ER_SUB(ER_FI[idx - 1], ER_FI[idx]), er_u64_to_double(s.next())),
-                        ER_FI[idx]);
+      double f = ER_ADD(ER_MUL(ER_SUB(ER_FI_AT(idx - 1), ER_FI_AT(idx)),
+                               er_u64_to_double(s.next())),
+                        ER_FI_AT(idx));
       if (s.exhausted()) return 0.0;
       if (f < exp(ER_MUL(ER_MUL(-0.5, x), x))) return x;
     }
