@@ -26,6 +26,19 @@
 //   * the value affine (value = alpha*stored + gamma, e.g. raw uint8 echo
 //     data with the z-score folded in) is applied once per particle in the
 //     finalize, so the gather moves 1 byte per corner for uint8 volumes.
+//
+// Build-time tuning flags (ER_NVCC_EXTRA="-DNAME=V"; the defaults are the
+// measured best on the B200, the alternatives are kept for the variant
+// scripts tools/variants*.sh and are recorded in profiles/README.md):
+//   ER_OCT_HALF=1          two rows per warp on 16-lane halves (0: one row, 32 lanes)
+//   ER_OCT_MINBLOCKS_F32=5 CTAs/SM for the fp32-class oct kernels (4: 62 regs; 6 spills)
+//   ER_OCT_SMEM_ACC=1      per-lane fp64 group accumulators in shared memory
+//   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2
+//   ER_FRAC_I2F=1          fractions by I2F on the fixed-point low word
+//   ER_OCT_TILE_MAJOR=1    tile-major CTA order (0: particle-major)
+//   ER_OCT_UNROLL=1        voxel-loop unroll; ER_OCT_LDPOLICY=0 (.nc; 1 .cg, 2 .cs)
+//   ER_OCT_THREADS=256     CTA size; ER_MIN_TILES=8 minimum tiles per particle
+//   ER_BOUNDS_CHECK=0      debug build: every gather index range-checked (common.cuh)
 #include "common.cuh"
 
 namespace {
