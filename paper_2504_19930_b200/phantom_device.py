@@ -60,23 +60,43 @@ def frame_axes(spec: PhantomSpec, k: int):
             tuple(a * scale for a in spec.inner_semiaxes))
 
 
-def frame_device(spec: PhantomSpec, k: int, speckle_dev, frame=True, mask=True, device=None):
-    """Frame k (f64) and its cavity mask (u8) as flat device tensors."""
+def frame_device(spec: PhantomSpec, k: int, speckle_dev, frame=True, mask=True, device=None,
+                 mask_out=None):
+    """Frame k (f64) and its cavity mask (u8) as flat device tensors (the mask
+    into ``mask_out`` when given)."""
     dev = require_cuda(device)
     t = torch()
     n = int(np.prod(spec.dims))
     f = t.empty(n, dtype=t.float64, device=dev) if frame else None
-    m = t.empty(n, dtype=t.uint8, device=dev) if mask else None
+    m = mask_out if mask_out is not None else (
+        t.empty(n, dtype=t.uint8, device=dev) if mask else None)
     outer, inner = frame_axes(spec, k)
     _lib.call("er_phantom_frame", ptr(speckle_dev) if frame else None,
               *(int(d) for d in spec.dims), _lib.d3(spec.spacing),
               _lib.d3(phantom_center(spec)), _lib.d3(outer), _lib.d3(inner),
-              ptr(f) if frame else None, ptr(m) if mask else None, stream_ptr(dev))
+              ptr(f) if frame else None, ptr(m) if m is not None else None, stream_ptr(dev))
     return f, m
 
 
+_PINNED = {}
+
+
+def _to_host(dev_u8) -> np.ndarray:
+    """Device bytes -> a fresh host array through a reused pinned staging
+    buffer (pageable device-to-host copies run at a fraction of the speed)."""
+    t = torch()
+    n = dev_u8.numel()
+    buf = _PINNED.get("u8")
+    if buf is None or buf.numel() < n:
+        buf = t.empty(n, dtype=t.uint8, pin_memory=True)
+        _PINNED["u8"] = buf
+    buf[:n].copy_(dev_u8.reshape(-1), non_blocking=True)
+    t.cuda.current_stream(dev_u8.device).synchronize()
+    return buf[:n].numpy().copy()
+
+
 def _host_u8(dev_u8, dims, spacing, origin=(0.0, 0.0, 0.0)) -> Volume3:
-    raw = dev_u8.reshape(dims).cpu().numpy()
+    raw = _to_host(dev_u8).reshape(dims)
     vol = Volume3.from_u8(raw, spacing, origin)
     adopt_u8(raw, dev_u8, dev_u8.device)
     return vol
@@ -130,17 +150,18 @@ def echo_case_device(dims=ECHO_DIMS, spacing=ECHO_SPACING, frames=1, seed=0, tru
     scale = 255.0 / _percentile_999(f0, spec.dims)
     del f0
     tq, sq, tm, sm = [], [], [], []
+    # the 8-bit results stay resident (they become the volumes' device
+    # copies): one allocation for all of them, sliced per frame
+    outs = t.empty((spec.frames, 4, n), dtype=t.uint8, device=dev)
     for k in range(spec.frames):
-        f, m = frame_device(spec, k, sp, device=dev)
-        u8 = t.empty(n, dtype=t.uint8, device=dev)
+        u8, su8, m, sm8 = outs[k]
+        f, _ = frame_device(spec, k, sp, device=dev, mask_out=m)
         _lib.call("er_quantize_u8", ptr(f), n, scale, n, ptr(u8), stream_ptr(dev))
         tq.append(_host_u8(u8, spec.dims, spec.spacing))
         moved = _resample_flat(f, _lib.ER_F64, spec.dims, a, b, dev)
-        su8 = t.empty(n, dtype=t.uint8, device=dev)
         _lib.call("er_quantize_u8", ptr(moved), n, scale, n, ptr(su8), stream_ptr(dev))
         sq.append(_host_u8(su8, spec.dims, spec.spacing))
         mm = _resample_flat(m, _lib.ER_U8, spec.dims, a, b, dev)
-        sm8 = t.empty(n, dtype=t.uint8, device=dev)
         _lib.call("er_binarize_u8", ptr(mm), n, 0.5, n, ptr(sm8), stream_ptr(dev))
         tm.append(_host_u8(m, spec.dims, spec.spacing))
         sm.append(_host_u8(sm8, spec.dims, spec.spacing))
