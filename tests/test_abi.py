@@ -80,3 +80,12 @@ def test_no_cpu_fallback_without_gpu():
     v = Volume3(np.zeros((4, 4, 4)))
     with pytest.raises(InternalError):
         Executor().measure_ncc(v, v, np.eye(4))
+
+
+def test_docs_state_the_entry_point_count():
+    """DESIGN.md and INTEGRATION.md quote the number of C-ABI entry points."""
+    n = len(declared_functions())
+    design = open(os.path.join(ROOT, "DESIGN.md"), encoding="utf-8").read()
+    integ = open(os.path.join(ROOT, "INTEGRATION.md"), encoding="utf-8").read()
+    assert re.search(r"(\d+) `extern \"C\"` entry points", design).group(1) == str(n)
+    assert re.search(r"all (\d+) entry", integ).group(1) == str(n)
