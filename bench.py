@@ -358,6 +358,7 @@ def run_ours(args):
         "post_ms_steps": [round(x, 3) for x in post_ms],
     }
     clk = clocks.summary()
+    modes = precision_modes(run, P, nvox, dev) if world == 1 else None
 
     # ---- e2e through the public API: fresh volumes each step, pinned uploads
     e2e = None
@@ -387,11 +388,37 @@ def run_ours(args):
                        "step": "one device SMC iteration (predict+affine+measure+update)",
                        "parallelism": f"particles sharded over {world} GPU(s)"},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "precision_modes": modes,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
     if launched:
         torch.distributed.destroy_process_group()
+
+
+def precision_modes(run, P, nvox, dev):
+    """Measurement-launch throughput of each sampling mode on the last
+    iteration's particles (after the timed region; one warm-up launch, then
+    one timed launch each, CUDA events on the launching stream): what the
+    parity-exact modes and the opt-in nearest-neighbour mode cost."""
+    import torch
+
+    from paper_2504_19930_b200 import ops
+
+    A, B = run.A[: run.plan.count], run.B[: run.plan.count]
+    out = {}
+    for mode in ("f32", "f64", "exact", "nearest"):
+        ops.measure(run.tdv, run.sdv, A, B, run.overlap, mode)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ops.measure(run.tdv, run.sdv, A, B, run.overlap, mode)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        out[mode] = {"evals_per_s": P * nvox / (ms * 1e-3), "ms": ms}
+    out["note"] = ("measurement launch only (not the bench step); f32 = default, f64 = "
+                   "parity-exact fast path, exact = reference op order, nearest = opt-in")
+    return out
 
 
 def run_plugin_seam(args, t, s, dev):
