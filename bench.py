@@ -16,9 +16,13 @@ CUDA events on the launching stream, max over ranks.
 ``e2e``: the same metric through the public API -- one ``register_smc`` call
 per step (50 iterations, the reference default) on fresh volume objects, so
 every step uploads both volumes from pinned host memory and reads the trace
-back.  ``--impl reference`` times the reference algorithm on the host CPU
-(the bit-exact C restatement in oracle/, all host threads) on a bounded
-particle sample of the same workload.
+back (also reported as ``registration_ms_per_pair``, BASELINE's second
+metric); ``e2e.plugin_seam``: the reference's kernel-module seam on its host
+fp64 arrays.  ``roofline``: the measurement kernel against the measured HBM
+(and L2) bandwidth; ``precision_modes``: one launch per sampling mode.
+``--impl reference`` times the reference algorithm on the host CPU (the
+bit-exact C restatement in oracle/, all host threads) on a bounded particle
+sample of the same workload.
 """
 
 from __future__ import annotations
@@ -51,7 +55,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--particles", type=int, default=2000)
-    ap.add_argument("--precision", default=None, help="f32 | f64 | exact")
+    ap.add_argument("--precision", default=None, help="f32 | f64 | exact | nearest")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
