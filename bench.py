@@ -80,6 +80,18 @@ def l2_roofline(achieved_gbs):
             "peak_source": "profiles/l2_bandwidth.json (tools/l2bw.cu, 52-96 MB resident)"}
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (recorded next to every CPU number)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return f"{line.split(':', 1)[1].strip()} ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return f"unknown ({os.cpu_count()} logical CPUs)"
+
+
 def make_workload():
     """Deterministic C2 inputs: normalised Volume3 pair with uint8 codec,
     generated on the GPU (phantom_device, byte-identical to the host
@@ -239,6 +251,7 @@ def run_reference(args):
         "config": {"workload": WORKLOAD, "particles_sampled": p, "voxels": nvox,
                    "host_threads": threads},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -376,6 +389,7 @@ def run_ours(args):
         a, b = first_iteration_affines(t, s, P)
         rate, sample_p, secs, threads = cpu_reference_rate(t, s, a, b, args.cpu_seconds)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "cpu_model": cpu_model(),
                "sample": (f"{sample_p} particles of SMC iteration 0 (C2 pair, full region) "
                           f"through the C oracle (bit-exact restatement of "
                           f"kernels_numba._ncc_kernel), {secs:.1f} s on {threads} host "

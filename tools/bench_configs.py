@@ -85,8 +85,11 @@ def c3():
     from paper_2504_19930_b200 import Executor, SmcConfig, register_sequence
     from paper_2504_19930_b200.phantom_device import echo_case_device
 
+    echo_case_device((40, 36, 44), frames=2)  # CUDA context + module load, not the generator
+    sync()
     t0 = time.perf_counter()
     case = echo_case_device(frames=30, seed=0)
+    sync()
     gen_s = time.perf_counter() - t0
     cfg = SmcConfig(mode="mask", n_particles=2000, n_iterations=50, seed=0)
     # warm-up on a 2-frame slice
@@ -95,6 +98,30 @@ def c3():
     register_sequence(Sequence4(case.target.frames[:2]), Sequence4(case.source.frames[:2]),
                       case.target_masks[:2], case.source_masks[:2],
                       SmcConfig(mode="mask", n_particles=64, n_iterations=2), Executor())
+    # stage times: the calls register_sequence makes, on
+    # a copy of the case with fresh raw arrays (so nothing is cached yet)
+    from paper_2504_19930_b200 import Volume3, binarize, register_smc, to_matrix
+    from paper_2504_19930_b200.pipeline import _normalize_frames, score_frames
+
+    def fresh(vols):
+        return [Volume3.from_u8(v.codec.raw.copy(), v.spacing, v.origin) for v in vols]
+
+    ft, fs = Sequence4(fresh(case.target.frames)), Sequence4(fresh(case.source.frames))
+    ftm, fsm = fresh(case.target_masks), fresh(case.source_masks)
+    stages = {}
+    t0 = time.perf_counter()
+    nt, ns = _normalize_frames(ft), _normalize_frames(fs)
+    sync()
+    stages["normalize_60_frames_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    reg_t, reg_s = binarize(ftm[0], 0.5), binarize(fsm[0], 0.5)
+    est, _ = register_smc(reg_t, reg_s, cfg, Executor(), trace_masks=(reg_t, reg_s))
+    sync()
+    stages["smc_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    score_frames(nt, ns, ftm, fsm, to_matrix(est, reg_t.physical_center()))
+    sync()
+    stages["warp_and_score_30_frames_s"] = time.perf_counter() - t0
     sync()
     t0 = time.perf_counter()
     rep = register_sequence(case.target, case.source, case.target_masks, case.source_masks,
@@ -102,7 +129,7 @@ def c3():
     sync()
     wall = time.perf_counter() - t0
     return {"config": "C3 mask SMC + 30-frame 4D warp/score, 176x176x208, 2000 x 50",
-            "register_sequence_s": wall, "phantom_generation_s": gen_s,
+            "register_sequence_s": wall, "stages": stages, "phantom_generation_s": gen_s,
             "dsc_before_mean": rep.aggregates["dsc_before_mean"],
             "dsc_after_mean": rep.aggregates["dsc_after_mean"],
             "ncc_after_mean": rep.aggregates["ncc_after_mean"],
