@@ -26,10 +26,24 @@ def lerp_code(precision: str) -> int:
         raise BadConfig(f"precision must be one of {sorted(LERP_MODES)}, got {precision!r}")
 
 
+def prepare_layouts(tdv: DeviceVolume, sdv: DeviceVolume, precision: str):
+    """Build (once) the source layout the measurement uses in this mode."""
+    if precision in ("f32", "nearest"):
+        sdv.ensure_fast_layout()       # bit-oct for binary sources, else oct
+    elif precision == "f64":
+        sdv.ensure_oct()
+
+
+def workspace_bytes(tdv: DeviceVolume, P: int) -> int:
+    return int(_lib.load().er_measure_workspace_bytes(tdv.desc_ptr, int(P)))
+
+
 def measure(tdv: DeviceVolume, sdv: DeviceVolume, A, B, overlap: bool, precision="f64",
-            out=None):
+            out=None, workspace=None):
     """Squared NCC per particle on device.  A: (P, 9) f64, B: (P, 3) f64 tensors.
-    Returns (ncc f64[P], degenerate u8[P], n_in i64[P]) device tensors."""
+    Returns (ncc f64[P], degenerate u8[P], n_in i64[P]) device tensors.
+    ``workspace``: a caller-owned uint8 scratch tensor (else the shared
+    per-device one, which concurrent streams must not share)."""
     t = torch()
     dev = A.device
     P = int(A.shape[0])
@@ -39,12 +53,12 @@ def measure(tdv: DeviceVolume, sdv: DeviceVolume, A, B, overlap: bool, precision
     ncc, degen, n_in = out
     if P == 0:
         return ncc, degen, n_in
-    if precision in ("f32", "nearest"):
-        sdv.ensure_fast_layout()       # bit-oct for binary sources, else oct
-    elif precision == "f64":
-        sdv.ensure_oct()
-    need = _lib.load().er_measure_workspace_bytes(tdv.desc_ptr, P)
-    ws = WORKSPACE.get(dev, need)
+    prepare_layouts(tdv, sdv, precision)
+    need = workspace_bytes(tdv, P)
+    if workspace is not None and workspace.numel() >= need:
+        ws = workspace
+    else:
+        ws = WORKSPACE.get(dev, need)
     _lib.call("er_measure_ncc", tdv.desc_ptr, sdv.desc_ptr, ptr(tdv.moments), ptr(A), ptr(B),
               P, int(bool(overlap)), lerp_code(precision), ptr(ncc), ptr(degen), ptr(n_in),
               ptr(ws), ws.numel(), stream_ptr(dev))

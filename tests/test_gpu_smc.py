@@ -264,3 +264,24 @@ def test_register_sequence_matches_reference():
     np.testing.assert_allclose(rep.dsc_after, g["dsc_after"], atol=1e-3)
     np.testing.assert_allclose(np.array(rep.trace["dsc"], dtype=float), g["trace_dsc"],
                                atol=1e-3)
+
+
+def test_register_smc_many_equals_one_at_a_time():
+    """Concurrent registrations (one stream each, interleaved iterations) give
+    exactly the per-pair register_smc results."""
+    from paper_2504_19930_b200 import (Executor, SmcConfig, normalize_zscore, register_smc,
+                                       register_smc_many)
+
+    g, tm, sm = _c1_volumes()
+    rng = np.random.default_rng(5)
+    it = normalize_zscore(type(tm)(tm.data + rng.random(tm.data.shape), tm.spacing))
+    isrc = normalize_zscore(type(sm)(sm.data + rng.random(sm.data.shape), sm.spacing))
+    pairs = [(tm, sm), (it, isrc), (sm, tm)]
+    mask_cfg = SmcConfig(mode="mask", n_particles=200, n_iterations=6, seed=3)
+    img_cfg = SmcConfig(n_particles=150, n_iterations=5, seed=1)
+    for cfg, ps in ((mask_cfg, [pairs[0], pairs[2]]), (img_cfg, [pairs[1], pairs[1]])):
+        many = register_smc_many(ps, cfg, Executor())
+        for (t, s), (est, tr) in zip(ps, many):
+            e1, tr1 = register_smc(t, s, cfg, Executor())
+            assert np.array_equal(est.to_array(), e1.to_array())
+            assert tr.ess == tr1.ess and tr.resampled == tr1.resampled
