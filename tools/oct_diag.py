@@ -1,3 +1,6 @@
+"""Oct fast path vs the C oracle on one of tests/test_gpu_oct.py's grid cases
+(anisotropic spacings, offset origins): per-precision relative error and
+count parity.  usage: oct_diag.py [case]  (GPU)"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

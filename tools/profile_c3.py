@@ -1,3 +1,5 @@
+"""cProfile of register_sequence on the C3 30-frame echo cycle (mask SMC
+2000 x 50 + warp/score of every frame), host-side view (GPU)."""
 import cProfile, os, pstats, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
