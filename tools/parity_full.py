@@ -18,7 +18,7 @@ if mode == "mask":
     from paper_2504_19930_b200 import binarize
     t, s = binarize(case.target_masks[0], 0.5), binarize(case.source_masks[0], 0.5)
 out = {"config": f"C2 shape, {mode} mode, {P} x {IT}", "seed": 0}
-for prec in ("f32", "exact"):
+for prec in ("f32", "f64", "exact"):
     t0 = time.perf_counter()
     est, tr = register_smc(t, s, SmcConfig(mode=mode, n_particles=P, n_iterations=IT, seed=0),
                            Executor(precision=prec))
@@ -34,7 +34,7 @@ oest, otr = osmc.register(t.data, s.data, geom, geom,
 out["cpu_s"] = time.perf_counter() - t0
 out["cpu_threads"] = ok.max_threads()
 out["cpu_estimate"] = oest.tolist()
-for prec in ("f32", "exact"):
+for prec in ("f32", "f64", "exact"):
     d = np.asarray(out[f"gpu_{prec}_estimate"]) - oest
     out[f"{prec}_max_rot_diff_deg"] = float(np.degrees(np.abs(d[:3])).max())
     out[f"{prec}_max_trans_diff_vox"] = float((np.abs(d[3:]) / np.asarray(t.spacing)).max())
