@@ -32,6 +32,7 @@
 // scripts tools/variants*.sh and are recorded in profiles/README.md):
 //   ER_OCT_HALF=1          two rows per warp on 16-lane halves (0: one row, 32 lanes)
 //   ER_OCT_MINBLOCKS_F32=5 CTAs/SM for the fp32-class oct kernels (4: 62 regs; 6 spills)
+//   ER_OCT_MINBLOCKS_F64=3 CTAs/SM for the fp64-lerp oct kernel
 //   ER_OCT_SMEM_ACC=1      per-lane fp64 group accumulators in shared memory
 //   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2
 //   ER_FRAC_I2F=1          fractions by I2F on the fixed-point low word
@@ -96,11 +97,14 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 #ifndef ER_OCT_MINBLOCKS_F32
 #define ER_OCT_MINBLOCKS_F32 5
 #endif
-// fp32 paths: keep the per-lane fp64 group accumulators in shared memory
-// (touched once per row) instead of 6 registers of the voxel loop
+#ifndef ER_OCT_MINBLOCKS_F64
+#define ER_OCT_MINBLOCKS_F64 3
+#endif
 #ifndef ER_MIN_TILES
 #define ER_MIN_TILES 8
 #endif
+// fp32 paths: keep the per-lane fp64 group accumulators in shared memory
+// (touched once per row) instead of 6 registers of the voxel loop
 #ifndef ER_OCT_SMEM_ACC
 #define ER_OCT_SMEM_ACC 1
 #endif
@@ -357,9 +361,11 @@ __device__ __forceinline__ float byte_magic(unsigned w, unsigned sel) {
   return __int_as_float(__byte_perm(w, 0x4B000000u, sel | 0x7650u));
 }
 
-__device__ __forceinline__ double byte_f64(unsigned w, unsigned sel) {
-  return __hiloint2double(0x43300000, __byte_perm(w, 0u, sel | 0x4440u)) - 4503599627370496.0;
+// 2^52 + byte as an exact double (no offset removed)
+__device__ __forceinline__ double byte_m64(unsigned w, unsigned sel) {
+  return __hiloint2double(0x43300000, __byte_perm(w, 0u, sel | 0x4440u));
 }
+
 
 // Fixed-point source coordinates with FB fractional bits.  FB = 32 (fp32
 // lerps): the integer part is the high register, the fraction the low one.
@@ -429,7 +435,8 @@ struct OctGeom {
 // BITS = 1: `oct` points at the bit-oct layout of a binary source (1 byte per
 // cell) and the lerps run in fp32 (row partials folded per row as below).
 template <typename TT, int LERP, int BITS = 0>
-__global__ void __launch_bounds__(kOctThreads, LERP != ER_LERP_F64 ? ER_OCT_MINBLOCKS_F32 : 3)
+__global__ void __launch_bounds__(kOctThreads,
+                                   LERP != ER_LERP_F64 ? ER_OCT_MINBLOCKS_F32 : ER_OCT_MINBLOCKS_F64)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
                        const OctGeom og, Partial* __restrict__ part) {
@@ -632,14 +639,16 @@ __global__ void __launch_bounds__(kOctThreads, LERP != ER_LERP_F64 ? ER_OCT_MINB
           pyx = fmaf(yf, x, pyx);
         } else {
           const double fu = F::frac64(cu), fv = F::frac64(cv), fw = F::frac64(cw);
-          const double x000 = byte_f64(c8.x, 0), x100 = byte_f64(c8.x, 1);
-          const double x010 = byte_f64(c8.x, 2), x110 = byte_f64(c8.x, 3);
-          const double x001 = byte_f64(c8.y, 0), x101 = byte_f64(c8.y, 1);
-          const double x011 = byte_f64(c8.y, 2), x111 = byte_f64(c8.y, 3);
-          const double c00 = fma(fu, x100 - x000, x000);
-          const double c10 = fma(fu, x110 - x010, x010);
-          const double c01 = fma(fu, x101 - x001, x001);
-          const double c11 = fma(fu, x111 - x011, x011);
+          // 2^52 + byte doubles: their differences are the exact byte
+          // differences, so only the four base corners need the offset removed
+          const double m000 = byte_m64(c8.x, 0), m100 = byte_m64(c8.x, 1);
+          const double m010 = byte_m64(c8.x, 2), m110 = byte_m64(c8.x, 3);
+          const double m001 = byte_m64(c8.y, 0), m101 = byte_m64(c8.y, 1);
+          const double m011 = byte_m64(c8.y, 2), m111 = byte_m64(c8.y, 3);
+          const double c00 = fma(fu, m100 - m000, m000 - 4503599627370496.0);
+          const double c10 = fma(fu, m110 - m010, m010 - 4503599627370496.0);
+          const double c01 = fma(fu, m101 - m001, m001 - 4503599627370496.0);
+          const double c11 = fma(fu, m111 - m011, m011 - 4503599627370496.0);
           const double c0 = fma(fv, c10 - c00, c00);
           const double c1 = fma(fv, c11 - c01, c01);
           const double x = fma(fw, c1 - c0, c0);
