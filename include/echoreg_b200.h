@@ -139,6 +139,16 @@ int er_smc_predict(const double *states_in_dev, double *states_out_dev, int64_t 
                    uint64_t seed, int64_t k, const double sigma[6], const double clip[6],
                    void *stream);
 
+/* er_smc_predict fused with er_states_to_affine for this rank's shard
+ * [first, first + count) of the predicted states: one launch per iteration
+ * instead of two; identical outputs. */
+int er_smc_predict_affine(const double *states_in_dev, double *states_out_dev, int64_t n,
+                          uint64_t seed, int64_t k, const double sigma[6], const double clip[6],
+                          int64_t first, int64_t count, const double center[3],
+                          const double tgt_spacing[3], const double tgt_origin[3],
+                          const double src_spacing[3], const double src_origin[3],
+                          double *A_dev, double *b_dev, void *stream);
+
 /* to_matrix about `center` (geometry.py:87-99) + index_affine
  * (geometry.py:136-152) for states [first, first + count). */
 int er_states_to_affine(const double *states_dev, int64_t first, int64_t count,

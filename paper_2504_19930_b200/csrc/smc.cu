@@ -120,13 +120,17 @@ struct Six {
 };
 
 // predict (smc.py:160-174)
+// A / B (optional): the index affines of particles [first, first + count)
+// computed from the freshly predicted state (fused er_states_to_affine)
 __global__ void smc_predict_kernel(const double* __restrict__ in, double* __restrict__ out,
                                    long long n, uint64_t seed, long long k, Six sigma,
-                                   Six clip) {
+                                   Six clip, long long first, long long count, AffineGeom g,
+                                   double* __restrict__ A, double* __restrict__ B) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   ErPhilox s;
   er_stream_init(&s, seed, 1, (uint64_t)k, (uint64_t)i);
+  double st[6];
 #pragma unroll 1
   for (int d = 0; d < 6; ++d) {
     const double z = er_standard_normal(&s);
@@ -134,7 +138,10 @@ __global__ void smc_predict_kernel(const double* __restrict__ in, double* __rest
     x = fmax(x, -clip.v[d]);
     x = fmin(x, clip.v[d]);
     out[6 * i + d] = x;
+    st[d] = x;
   }
+  if (A && i >= first && i < first + count)
+    state_to_affine(st, g, A + 9 * (i - first), B + 3 * (i - first));
 }
 
 // ---- single-CTA update: weights, ESS, systematic resampling, estimate ----
@@ -447,7 +454,35 @@ extern "C" int er_smc_predict(const double* states_in_dev, double* states_out_de
     cl.v[d] = clip[d];
   }
   smc_predict_kernel<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(
-      states_in_dev, states_out_dev, n, seed, k, sg, cl);
+      states_in_dev, states_out_dev, n, seed, k, sg, cl, 0, 0, AffineGeom{}, nullptr, nullptr);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_smc_predict_affine(const double* states_in_dev, double* states_out_dev,
+                                     int64_t n, uint64_t seed, int64_t k, const double sigma[6],
+                                     const double clip[6], int64_t first, int64_t count,
+                                     const double center[3], const double tgt_spacing[3],
+                                     const double tgt_origin[3], const double src_spacing[3],
+                                     const double src_origin[3], double* A_dev, double* b_dev,
+                                     void* stream) {
+  if (!states_in_dev || !states_out_dev || !sigma || !clip || n < 0 || first < 0 ||
+      count < 0 || first + count > n || (count > 0 && (!A_dev || !b_dev)))
+    return er_set_error(ER_EINVAL, "er_smc_predict_affine: args");
+  if (n == 0) return ER_OK;
+  Six sg, cl;
+  for (int d = 0; d < 6; ++d) {
+    sg.v[d] = sigma[d];
+    cl.v[d] = clip[d];
+  }
+  if (count > 0 && (!center || !tgt_spacing || !tgt_origin || !src_spacing || !src_origin))
+    return er_set_error(ER_EINVAL, "er_smc_predict_affine: geometry");
+  const AffineGeom g = count > 0 ? make_affine_geom(center, tgt_spacing, tgt_origin,
+                                                    src_spacing, src_origin)
+                                 : AffineGeom{};
+  smc_predict_kernel<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(
+      states_in_dev, states_out_dev, n, seed, k, sg, cl, first, count, g,
+      count > 0 ? A_dev : nullptr, b_dev);
   ER_CHECK_LAUNCH();
   return ER_OK;
 }

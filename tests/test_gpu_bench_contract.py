@@ -46,7 +46,7 @@ def test_bench_line_contract():
     assert e["plugin_seam"]["value"] > 0 and e["plugin_seam"]["cold"]["value"] > 0
     k = d["clocks"]
     assert k["sm_mhz"] > 0 and isinstance(k["reasons"], list)
-    assert d["gpu_launches"] >= 5 * 3  # predict, affine, measure x2, update per step
+    assert d["gpu_launches"] >= 4 * 3  # predict+affine, measure x2, update per step
 
 
 def test_reference_arm_line_contract():
