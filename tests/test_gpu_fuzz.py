@@ -19,3 +19,11 @@ def test_random_cases_match_the_oracle(seed):
 
     res = fuzz_measure.run(n_cases=40, seed=seed)
     assert not res["failures"], res["failures"][:5]
+
+
+def test_random_warp_cases_match_the_oracle():
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import fuzz_measure
+
+    res = fuzz_measure.run_warp(n_cases=40, seed=3)
+    assert not res["failures"], res["failures"][:5]
