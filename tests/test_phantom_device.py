@@ -133,3 +133,35 @@ def test_phantom_abi_rejects_bad_arguments():
     with pytest.raises(BadConfig):
         _lib.call("er_phantom_frame", None, 0, 4, 4, _lib.d3((1, 1, 1)), _lib.d3((0, 0, 0)),
                   _lib.d3((1, 1, 1)), _lib.d3((1, 1, 1)), None, None, None)
+
+
+@gpu
+def test_random_phantom_specs_match_the_host_generator():
+    """make_phantom_device == make_phantom (the reference's algorithm) bit for
+    bit over random specs: dims, frames, semi-axes, amplitude, speckle sigma,
+    spacing, centre, seed."""
+    from numpy._core._multiarray_umath import __cpu_features__
+
+    if not __cpu_features__.get("AVX512_SKX"):
+        pytest.skip("host np.exp is not the SVML variant the device restates")
+    from paper_2504_19930_b200 import PhantomSpec, make_phantom
+    from paper_2504_19930_b200.phantom_device import make_phantom_device
+
+    g = np.random.default_rng(2504)
+    for _ in range(12):
+        dims = tuple(int(x) for x in g.integers(4, 33, 3))
+        outer = tuple(float(x) for x in g.uniform(3.0, 14.0, 3))
+        inner = tuple(float(o * f) for o, f in zip(outer, g.uniform(0.3, 0.9, 3)))
+        spec = PhantomSpec(dims=dims, spacing=tuple(float(x) for x in g.uniform(0.6, 1.4, 3)),
+                           outer_semiaxes=outer, inner_semiaxes=inner,
+                           center=None if g.random() < 0.5 else
+                           tuple(float(x) for x in g.uniform(-2.0, 20.0, 3)),
+                           speckle_sigma=float(g.choice([0.0, 0.2, 0.3, 0.7])),
+                           amplitude=float(g.uniform(0.0, 0.5)),
+                           frames=int(g.integers(1, 5)), seed=int(g.integers(0, 2**40)))
+        hs, hm = make_phantom(spec)
+        ds, dm = make_phantom_device(spec)
+        for a, b in zip(hs.frames, ds.frames):
+            assert np.array_equal(a.data, b.data), spec
+        for a, b in zip(hm, dm):
+            assert np.array_equal(a.codec.raw, b.codec.raw), spec
