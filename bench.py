@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-modes", action="store_true", help="skip the per-precision-mode launches")
     return ap.parse_args()
 
 
@@ -375,7 +376,7 @@ def run_ours(args):
         "post_ms_steps": [round(x, 3) for x in post_ms],
     }
     clk = clocks.summary()
-    modes = precision_modes(run, P, nvox, dev) if world == 1 else None
+    modes = precision_modes(run, P, nvox, dev) if world == 1 and not args.no_modes else None
 
     # ---- e2e through the public API: fresh volumes each step, pinned uploads
     e2e = None
