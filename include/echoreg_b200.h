@@ -91,6 +91,17 @@ int er_build_bitoct(const er_volume *v, void *bitoct_dev, void *stream);
  * it (exact integer sums -> numpy-identical mean).  hist_dev: 256 int64. */
 int er_histogram_u8(const er_volume *v, int64_t *hist_dev, void *stream);
 
+/* Ingest of an 8-bit NIfTI payload (E/io.py:124-187, the reader's
+ * reshape(order="F") at io.py:165-171): payload_dev holds frames x nz x ny x
+ * nx bytes as on disk (x fastest, frame slowest); out_dev receives the frames
+ * in the reference's memory order (each (nx, ny, nz) C order, z fastest),
+ * frame f at out_dev + f*nx*ny*nz.  hist_dev (frames x 256 int64, or NULL)
+ * receives each frame's exact 256-bin histogram, from which the z-score of
+ * volume.py:119-130 is computed (same counts as er_histogram_u8).  One launch
+ * (plus a zeroing launch when hist_dev is set).  frames <= 65535. */
+int er_ingest_u8(const uint8_t *payload_dev, int64_t nx, int64_t ny, int64_t nz, int64_t frames,
+                 uint8_t *out_dev, int64_t *hist_dev, void *stream);
+
 /* Classify an f64 device volume: flags_dev[0] = 1 if every voxel is 0 or 1
  * (volume.py:138-140), flags_dev[1] = 1 if every voxel is exactly
  * representable in fp32.  Used to pick a lossless storage type. */

@@ -178,6 +178,104 @@ __global__ void lattice_kernel(const double* __restrict__ v, long long n, double
   if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicAnd(flags, 0);
 }
 
+
+// ---- ingest of an 8-bit NIfTI payload (E/io.py:165-171) --------------------
+// On disk the voxels are x fastest, frame slowest; in memory a Volume3 is
+// (nx, ny, nz) C order, k (z) fastest (E/volume.py:20-33).  For each (frame,
+// y) plane this is a 2D transpose of the (z, x) byte plane: 64 x 64 tiles
+// staged in shared memory, read and written as 32-bit words (16 lanes per
+// 64-byte row) when rows are word-aligned, bytes otherwise; the next plane's
+// words are prefetched into registers while the current plane is stored.
+// The per-frame 256-bin histogram of volume.py:119-130's z-score (exact
+// integer counts) is accumulated in the same pass: shared-memory bins per
+// block, one global atomic per non-empty bin.
+constexpr int kIngT = 64;
+constexpr int kIngPitch = 68;  // bytes per shared row; a multiple of 4 for word stores
+
+__device__ __forceinline__ unsigned int ingest_load(const uint8_t* __restrict__ fin, long long plane,
+                                                    int nx, int nz, int x, int z, int y,
+                                                    bool words_in) {
+  if (z >= nz) return 0u;
+  const uint8_t* src = fin + (long long)z * plane + (long long)y * nx + x;
+  // with nx % 4 == 0 a 4-byte word is either wholly inside the row or wholly outside
+  if (words_in) return x < nx ? __ldg(reinterpret_cast<const unsigned int*>(src)) : 0u;
+  unsigned int w = 0u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (x + i < nx) w |= (unsigned int)__ldg(src + i) << (8 * i);
+  return w;
+}
+
+__global__ void __launch_bounds__(256)
+    ingest_u8_kernel(const uint8_t* __restrict__ in, int nx, int ny, int nz, int tiles_x,
+                     int y_per_block, bool words_in, bool words_out, uint8_t* __restrict__ out,
+                     unsigned long long* __restrict__ hist) {
+  __shared__ __align__(16) uint8_t tile[kIngT * kIngPitch];
+  __shared__ unsigned int h[256];
+  const int t = threadIdx.x;
+  const int x0 = (blockIdx.x % tiles_x) * kIngT, z0 = (blockIdx.x / tiles_x) * kIngT;
+  const long long plane = (long long)nx * ny;
+  const long long vol = plane * nz;
+  const uint8_t* fin = in + (long long)blockIdx.z * vol;
+  uint8_t* fout = out + (long long)blockIdx.z * vol;
+  if (hist) h[t] = 0u;
+  const int c4 = (t & 15) * 4, r0 = t >> 4;  // 16 words per 64-byte row, 16 rows per pass
+  const int y_lo = blockIdx.y * y_per_block;
+  const int y_hi = min(ny, y_lo + y_per_block);
+  // register prefetch: plane y+1's words are in flight while plane y is stored
+  unsigned int cur[4], nxt[4];
+  if (y_lo < y_hi) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+      cur[p] = ingest_load(fin, plane, nx, nz, x0 + c4, z0 + r0 + 16 * p, y_lo, words_in);
+  }
+  const bool zw = words_out && (z0 + c4 + 4 <= nz);  // a whole output word in the row
+  for (int y = y_lo; y < y_hi; ++y) {
+    if (y + 1 < y_hi) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+        nxt[p] = ingest_load(fin, plane, nx, nz, x0 + c4, z0 + r0 + 16 * p, y + 1, words_in);
+    }
+    __syncthreads();  // the previous plane's transposed reads are done with the tile
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+      *reinterpret_cast<unsigned int*>(&tile[(r0 + 16 * p) * kIngPitch + c4]) = cur[p];
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r = r0 + 16 * p;
+      const int x = x0 + r;
+      if (x >= nx) continue;
+      unsigned int w = 0u;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w |= (unsigned int)tile[(c4 + i) * kIngPitch + r] << (8 * i);
+      uint8_t* dst = fout + ((long long)x * ny + y) * nz + z0 + c4;
+      if (zw) {
+        *reinterpret_cast<unsigned int*>(dst) = w;
+        if (hist) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) atomicAdd(&h[(w >> (8 * i)) & 255u], 1u);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (z0 + c4 + i < nz) {
+            const unsigned int b = (w >> (8 * i)) & 255u;
+            dst[i] = (uint8_t)b;
+            if (hist) atomicAdd(&h[b], 1u);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) cur[p] = nxt[p];
+  }
+  if (hist) {
+    __syncthreads();
+    if (h[t]) atomicAdd(&hist[256ull * blockIdx.z + t], (unsigned long long)h[t]);
+  }
+}
+
 template <typename T>
 void launch_moments(const void* data, long long n, double* part, cudaStream_t st) {
   moments_partial_kernel<T><<<kMomBlocks, kMomThreads, 0, st>>>((const T*)data, n, part);
@@ -282,3 +380,37 @@ extern "C" int er_histogram_u8(const er_volume* v, int64_t* hist_dev, void* stre
 }
 
 ER_DEFINE_FAULT_READER(er_faults_volume)
+
+extern "C" int er_ingest_u8(const uint8_t* payload_dev, int64_t nx, int64_t ny, int64_t nz,
+                            int64_t frames, uint8_t* out_dev, int64_t* hist_dev, void* stream) {
+  if (!payload_dev || !out_dev || nx < 1 || ny < 1 || nz < 1 || frames < 0)
+    return er_set_error(ER_EINVAL, "er_ingest_u8: args");
+  if (nx > INT32_MAX || ny > INT32_MAX || nz > INT32_MAX || frames > 65535)
+    return er_set_error(ER_EINVAL, "er_ingest_u8: dims out of range");
+  if ((const void*)payload_dev == (const void*)out_dev)
+    return er_set_error(ER_EINVAL, "er_ingest_u8: in-place reorder is not supported");
+  cudaStream_t st = as_stream(stream);
+  if (hist_dev && frames > 0)
+    zero_u64_kernel<<<1, 256, 0, st>>>((unsigned long long*)hist_dev, 256 * frames);
+  if (frames == 0) {
+    ER_CHECK_LAUNCH();
+    return ER_OK;
+  }
+  const int tiles_x = (int)((nx + kIngT - 1) / kIngT), tiles_z = (int)((nz + kIngT - 1) / kIngT);
+  const long long tiles = (long long)tiles_x * tiles_z;
+  if (tiles > INT32_MAX) return er_set_error(ER_EINVAL, "er_ingest_u8: dims out of range");
+  // split y into ~4 waves of 8 blocks per SM (short tail); each block walks its y range
+  long long chunks = (ER_NUM_SMS_B200 * 32 + tiles * frames - 1) / (tiles * frames);
+  if (chunks < 1) chunks = 1;
+  if (chunks > ny) chunks = ny;
+  const int y_per_block = (int)((ny + chunks - 1) / chunks);
+  chunks = (ny + y_per_block - 1) / y_per_block;
+  const bool words_in = (nx % 4 == 0) && (reinterpret_cast<uintptr_t>(payload_dev) % 4 == 0);
+  const bool words_out = (nz % 4 == 0) && (reinterpret_cast<uintptr_t>(out_dev) % 4 == 0);
+  dim3 grid((unsigned)tiles, (unsigned)chunks, (unsigned)frames);
+  ingest_u8_kernel<<<grid, 256, 0, st>>>(payload_dev, (int)nx, (int)ny, (int)nz, tiles_x,
+                                         y_per_block, words_in, words_out, out_dev,
+                                         (unsigned long long*)hist_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
