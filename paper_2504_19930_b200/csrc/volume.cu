@@ -182,15 +182,17 @@ __global__ void lattice_kernel(const double* __restrict__ v, long long n, double
 // ---- ingest of an 8-bit NIfTI payload (E/io.py:165-171) --------------------
 // On disk the voxels are x fastest, frame slowest; in memory a Volume3 is
 // (nx, ny, nz) C order, k (z) fastest (E/volume.py:20-33).  For each (frame,
-// y) plane this is a 2D transpose of the (z, x) byte plane: 64 x 64 tiles
-// staged in shared memory, read and written as 32-bit words (16 lanes per
-// 64-byte row) when rows are word-aligned, bytes otherwise; the next plane's
-// words are prefetched into registers while the current plane is stored.
-// The per-frame 256-bin histogram of volume.py:119-130's z-score (exact
-// integer counts) is accumulated in the same pass: shared-memory bins per
-// block, one global atomic per non-empty bin.
+// y) plane this is a 2D transpose of the (z, x) byte plane, done in 64 x 64
+// tiles: each thread loads a 4 x 4 byte block (4 rows z, one 32-bit word of
+// x; 16 lanes cover a 64-byte row), transposes it in registers with PRMT and
+// writes 4 words of 4 z-consecutive bytes into an XOR-swizzled shared tile,
+// from which whole output words are read back (conflict-free) and stored
+// coalesced.  Rows that are not word-aligned take byte loads / stores.  The
+// next plane's block is prefetched into registers while the current plane
+// is stored.  The per-frame 256-bin histogram of volume.py:119-130's z-score
+// (exact integer counts) is accumulated in the same pass: shared-memory bins
+// per block, one global atomic per non-empty bin.
 constexpr int kIngT = 64;
-constexpr int kIngPitch = 68;  // bytes per shared row; a multiple of 4 for word stores
 
 __device__ __forceinline__ unsigned int ingest_load(const uint8_t* __restrict__ fin, long long plane,
                                                     int nx, int nz, int x, int z, int y,
@@ -206,11 +208,14 @@ __device__ __forceinline__ unsigned int ingest_load(const uint8_t* __restrict__ 
   return w;
 }
 
+// shared word of (local x, z word): 16 words per x row, XOR-swizzled by x / 4
+__device__ __forceinline__ int ingest_slot(int xl, int zw) { return xl * 16 + (zw ^ (xl >> 2)); }
+
 __global__ void __launch_bounds__(256)
     ingest_u8_kernel(const uint8_t* __restrict__ in, int nx, int ny, int nz, int tiles_x,
                      int y_per_block, bool words_in, bool words_out, uint8_t* __restrict__ out,
                      unsigned long long* __restrict__ hist) {
-  __shared__ __align__(16) uint8_t tile[kIngT * kIngPitch];
+  __shared__ unsigned int tile[kIngT * 16];
   __shared__ unsigned int h[256];
   const int t = threadIdx.x;
   const int x0 = (blockIdx.x % tiles_x) * kIngT, z0 = (blockIdx.x / tiles_x) * kIngT;
@@ -219,38 +224,43 @@ __global__ void __launch_bounds__(256)
   const uint8_t* fin = in + (long long)blockIdx.z * vol;
   uint8_t* fout = out + (long long)blockIdx.z * vol;
   if (hist) h[t] = 0u;
-  const int c4 = (t & 15) * 4, r0 = t >> 4;  // 16 words per 64-byte row, 16 rows per pass
+  const int xw = t & 15, zq = t >> 4;  // load role: x word, z quad
+  const int zw = t & 15, xr = t >> 4;  // store role: z word, x row
   const int y_lo = blockIdx.y * y_per_block;
   const int y_hi = min(ny, y_lo + y_per_block);
-  // register prefetch: plane y+1's words are in flight while plane y is stored
   unsigned int cur[4], nxt[4];
   if (y_lo < y_hi) {
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
-      cur[p] = ingest_load(fin, plane, nx, nz, x0 + c4, z0 + r0 + 16 * p, y_lo, words_in);
+    for (int j = 0; j < 4; ++j)
+      cur[j] = ingest_load(fin, plane, nx, nz, x0 + 4 * xw, z0 + 4 * zq + j, y_lo, words_in);
   }
-  const bool zw = words_out && (z0 + c4 + 4 <= nz);  // a whole output word in the row
+  const int zs = z0 + 4 * zw;
+  const bool zfull = words_out && (zs + 4 <= nz);  // a whole output word inside the row
   for (int y = y_lo; y < y_hi; ++y) {
     if (y + 1 < y_hi) {
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
-        nxt[p] = ingest_load(fin, plane, nx, nz, x0 + c4, z0 + r0 + 16 * p, y + 1, words_in);
+      for (int j = 0; j < 4; ++j)
+        nxt[j] = ingest_load(fin, plane, nx, nz, x0 + 4 * xw, z0 + 4 * zq + j, y + 1, words_in);
     }
-    __syncthreads();  // the previous plane's transposed reads are done with the tile
-#pragma unroll
-    for (int p = 0; p < 4; ++p)
-      *reinterpret_cast<unsigned int*>(&tile[(r0 + 16 * p) * kIngPitch + c4]) = cur[p];
+    // 4 x 4 byte transpose: o[i] = byte i of cur[0..3] (x = 4 xw + i, z = 4 zq .. 4 zq + 3)
+    const unsigned int a = __byte_perm(cur[0], cur[1], 0x5140);
+    const unsigned int b = __byte_perm(cur[2], cur[3], 0x5140);
+    const unsigned int c = __byte_perm(cur[0], cur[1], 0x7362);
+    const unsigned int d = __byte_perm(cur[2], cur[3], 0x7362);
+    __syncthreads();  // the previous plane's reads are done with the tile
+    tile[ingest_slot(4 * xw + 0, zq)] = __byte_perm(a, b, 0x5410);
+    tile[ingest_slot(4 * xw + 1, zq)] = __byte_perm(a, b, 0x7632);
+    tile[ingest_slot(4 * xw + 2, zq)] = __byte_perm(c, d, 0x5410);
+    tile[ingest_slot(4 * xw + 3, zq)] = __byte_perm(c, d, 0x7632);
     __syncthreads();
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-      const int r = r0 + 16 * p;
-      const int x = x0 + r;
-      if (x >= nx) continue;
-      unsigned int w = 0u;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) w |= (unsigned int)tile[(c4 + i) * kIngPitch + r] << (8 * i);
-      uint8_t* dst = fout + ((long long)x * ny + y) * nz + z0 + c4;
-      if (zw) {
+      const int xl = xr + 16 * p;
+      const int x = x0 + xl;
+      if (x >= nx || zs >= nz) continue;
+      const unsigned int w = tile[ingest_slot(xl, zw)];
+      uint8_t* dst = fout + ((long long)x * ny + y) * nz + zs;
+      if (zfull) {
         *reinterpret_cast<unsigned int*>(dst) = w;
         if (hist) {
 #pragma unroll
@@ -259,16 +269,16 @@ __global__ void __launch_bounds__(256)
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          if (z0 + c4 + i < nz) {
-            const unsigned int b = (w >> (8 * i)) & 255u;
-            dst[i] = (uint8_t)b;
-            if (hist) atomicAdd(&h[b], 1u);
+          if (zs + i < nz) {
+            const unsigned int v = (w >> (8 * i)) & 255u;
+            dst[i] = (uint8_t)v;
+            if (hist) atomicAdd(&h[v], 1u);
           }
         }
       }
     }
 #pragma unroll
-    for (int p = 0; p < 4; ++p) cur[p] = nxt[p];
+    for (int j = 0; j < 4; ++j) cur[j] = nxt[j];
   }
   if (hist) {
     __syncthreads();
