@@ -195,16 +195,17 @@ __global__ void lattice_kernel(const double* __restrict__ v, long long n, double
 constexpr int kIngT = 64;
 
 __device__ __forceinline__ unsigned int ingest_load(const uint8_t* __restrict__ fin, long long plane,
-                                                    int nx, int nz, int x, int z, int y,
-                                                    bool words_in) {
+                                                    long long vol, int nx, int nz, int x, int z,
+                                                    int y, bool words_in) {
   if (z >= nz) return 0u;
-  const uint8_t* src = fin + (long long)z * plane + (long long)y * nx + x;
+  const long long q = (long long)z * plane + (long long)y * nx + x;
   // with nx % 4 == 0 a 4-byte word is either wholly inside the row or wholly outside
-  if (words_in) return x < nx ? __ldg(reinterpret_cast<const unsigned int*>(src)) : 0u;
+  if (words_in)
+    return x < nx ? __ldg(reinterpret_cast<const unsigned int*>(fin + er_idx(q, vol - 3))) : 0u;
   unsigned int w = 0u;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-    if (x + i < nx) w |= (unsigned int)__ldg(src + i) << (8 * i);
+    if (x + i < nx) w |= (unsigned int)__ldg(fin + er_idx(q + i, vol)) << (8 * i);
   return w;
 }
 
@@ -232,7 +233,8 @@ __global__ void __launch_bounds__(256)
   if (y_lo < y_hi) {
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      cur[j] = ingest_load(fin, plane, nx, nz, x0 + 4 * xw, z0 + 4 * zq + j, y_lo, words_in);
+      cur[j] = ingest_load(fin, plane, vol, nx, nz, x0 + 4 * xw, z0 + 4 * zq + j, y_lo,
+                           words_in);
   }
   const int zs = z0 + 4 * zw;
   const bool zfull = words_out && (zs + 4 <= nz);  // a whole output word inside the row
@@ -240,7 +242,8 @@ __global__ void __launch_bounds__(256)
     if (y + 1 < y_hi) {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        nxt[j] = ingest_load(fin, plane, nx, nz, x0 + 4 * xw, z0 + 4 * zq + j, y + 1, words_in);
+        nxt[j] = ingest_load(fin, plane, vol, nx, nz, x0 + 4 * xw, z0 + 4 * zq + j, y + 1,
+                             words_in);
     }
     // 4 x 4 byte transpose: o[i] = byte i of cur[0..3] (x = 4 xw + i, z = 4 zq .. 4 zq + 3)
     const unsigned int a = __byte_perm(cur[0], cur[1], 0x5140);
@@ -259,9 +262,10 @@ __global__ void __launch_bounds__(256)
       const int x = x0 + xl;
       if (x >= nx || zs >= nz) continue;
       const unsigned int w = tile[ingest_slot(xl, zw)];
-      uint8_t* dst = fout + ((long long)x * ny + y) * nz + zs;
+      const long long q = ((long long)x * ny + y) * nz + zs;
+      uint8_t* dst = fout + q;
       if (zfull) {
-        *reinterpret_cast<unsigned int*>(dst) = w;
+        *reinterpret_cast<unsigned int*>(fout + er_idx(q, vol - 3)) = w;
         if (hist) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) atomicAdd(&h[(w >> (8 * i)) & 255u], 1u);
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(256)
         for (int i = 0; i < 4; ++i) {
           if (zs + i < nz) {
             const unsigned int v = (w >> (8 * i)) & 255u;
-            dst[i] = (uint8_t)v;
+            dst[er_idx(i, vol - q)] = (uint8_t)v;
             if (hist) atomicAdd(&h[v], 1u);
           }
         }

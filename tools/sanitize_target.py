@@ -1,16 +1,18 @@
 """Small end-to-end exercise of every kernel family, for compute-sanitizer
 (one tool per run): generic measurement (f32/f64 storage, 3 precisions),
 oct (u8) and bit-oct (binary) fast paths in full and overlap mode, odd
-shapes, predict/update, exhaustive grid, warps, Dice, NCC, histogram."""
+shapes, predict/update, exhaustive grid, warps, Dice, NCC, histogram, 8-bit
+NIfTI ingest (word and byte paths, partial tiles, several frames)."""
 import os
 import sys
+import tempfile
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2504_19930_b200 import (Executor, GridSpec, RigidParams, SmcConfig, Volume3,  # noqa: E402
-                                   dice, dice_under_transform, ncc, normalize_zscore,
+from paper_2504_19930_b200 import (Executor, GridSpec, RigidParams, Sequence4,  # noqa: E402
+                                   SmcConfig, Volume3, dice, dice_under_transform, ncc, normalize_zscore,
                                    register_exhaustive, register_smc, resample, to_matrix)
 
 rng = np.random.default_rng(0)
@@ -40,6 +42,14 @@ for dims in ((9, 7, 11), (5, 1, 6), (1, 4, 4), (17, 13, 19)):
                                  ncc_region="overlap"), trace_masks=(m, m))
     register_exhaustive(img, img, GridSpec(half_counts=(1, 0, 1, 0, 1, 1), step_t=1.0,
                                            step_r=3.0))
+from paper_2504_19930_b200.io import read_volume_device, write_u8_nifti  # noqa: E402
+
+with tempfile.TemporaryDirectory() as d:
+    for dims, nf in (((9, 7, 11), 3), ((68, 5, 130), 2), ((64, 3, 64), 1), ((1, 1, 1), 1)):
+        seq = Sequence4([Volume3.from_u8(rng.integers(0, 256, dims).astype(np.uint8))
+                         for _ in range(nf)])
+        write_u8_nifti(seq, os.path.join(d, "v.nii"))
+        read_volume_device(os.path.join(d, "v.nii"))
 torch.cuda.synchronize()
 print("sanitize target done")
 from paper_2504_19930_b200 import _lib  # noqa: E402
