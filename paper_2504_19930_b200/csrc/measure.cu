@@ -923,9 +923,11 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
     return er_set_error(ER_EINVAL, "er_measure_ncc: too many particles for one launch");
   cudaStream_t st = as_stream(stream);
   Partial* part = (Partial*)workspace_dev;
-  // (the oct kernel's per-tile group slots assume a tile of <= kRowsPerTile rows)
-  // (the oct kernels' per-tile group slots assume a tile of <= kRowsPerTile rows)
-  const bool fast = lerp_mode != ER_LERP_EXACT && tgt->ny <= kRowsPerTile && src->dtype == ER_U8;
+  // (the oct kernels' per-tile group slots assume a tile of <= kRowsPerTile rows,
+  // and their 32-bit cell indices a padded source grid of < 2^31 cells)
+  const long long cells = (long long)(src->nx + 1) * (src->ny + 1) * (src->nz + 1);
+  const bool fast = lerp_mode != ER_LERP_EXACT && tgt->ny <= kRowsPerTile &&
+                    src->dtype == ER_U8 && cells < (1LL << 31);
   const bool use_bits =
       fast && (lerp_mode == ER_LERP_F32 || lerp_mode == ER_LERP_NEAREST) && src->bitoct_dev;
   const bool use_oct = fast && !use_bits && src->oct_dev;

@@ -83,10 +83,18 @@ class DeviceVolume:
     def nbytes(self) -> int:
         return int(self.storage.numel() * self.storage.element_size())
 
+    def fast_layout_fits(self) -> bool:
+        """The fast kernels index padded cells in 32 bits: a padded grid of
+        >= 2^31 cells (only thin volumes, given < 2^31 voxels) gets no fast
+        layout and takes the generic gather kernel (er_measure_ncc decides
+        the same way)."""
+        nx, ny, nz = self.dims
+        return (nx + 1) * (ny + 1) * (nz + 1) < 2**31
+
     def ensure_oct(self):
         """Build (once per 8-bit array) the oct re-layout used by the
         measurement fast path: all 8 trilinear corners of a cell in 8 bytes."""
-        if self.dtype_code != _lib.ER_U8 or self.desc.oct_dev:
+        if self.dtype_code != _lib.ER_U8 or self.desc.oct_dev or not self.fast_layout_fits():
             return
         sh = self.shared
         if sh is None or sh.oct is None:
@@ -114,7 +122,7 @@ class DeviceVolume:
     def ensure_bitoct(self):
         """Build (once per 8-bit array) the bit-oct re-layout of a binary
         source: the 8 corner bits of a cell in one byte (mask fast path)."""
-        if self.desc.bitoct_dev:
+        if self.desc.bitoct_dev or not self.fast_layout_fits():
             return
         sh = self.shared
         lay = getattr(sh, "bitoct", None) if sh is not None else getattr(self, "bitoct", None)
