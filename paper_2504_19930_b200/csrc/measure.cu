@@ -35,6 +35,8 @@
 //   ER_OCT_MINBLOCKS_F64=3 CTAs/SM for the fp64-lerp oct kernel
 //   ER_OCT_SMEM_ACC=1      per-lane fp64 group accumulators in shared memory
 //   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2
+//   ER_OCT_ACC2=1          px += x; (pxx, pyx) by one FFMA2 of x * (x, y)
+//                          (0: (px, pxx) by FFMA2 of x * (1, x), 2 more SASS)
 //   ER_FRAC_I2F=1          fractions by I2F on the fixed-point low word
 //   ER_OCT_TILE_MAJOR=1    tile-major CTA order (0: particle-major)
 //   ER_OCT_UNROLL=1        voxel-loop unroll; ER_OCT_LDPOLICY=0 (.nc; 1 .cg, 2 .cs)
@@ -112,6 +114,26 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 #ifndef ER_OCT_FMUL2
 #define ER_OCT_FMUL2 1
 #endif
+// fp32 paths: accumulate as px += x and (pxx, pyx) += x * (x, y) (one FADD +
+// one FFMA2 whose operand pair is two computed values, no 1.0f constant)
+#ifndef ER_OCT_ACC2
+#define ER_OCT_ACC2 1
+#endif
+
+// per-voxel fp32 row partials: sum x, sum x^2, sum y*x (both forms round identically)
+__device__ __forceinline__ void acc_voxel(float x, float yf, float& px, float& pxx, float& pyx) {
+#if ER_OCT_ACC2
+  px += x;
+  const float2 a = __ffma2_rn(make_float2(x, x), make_float2(x, yf), make_float2(pxx, pyx));
+  pxx = a.x;
+  pyx = a.y;
+#else
+  const float2 a = __ffma2_rn(make_float2(x, x), make_float2(1.0f, x), make_float2(px, pxx));
+  px = a.x;
+  pxx = a.y;
+  pyx = fmaf(yf, x, pyx);
+#endif
+}
 
 
 // kernels_numba.py:88-113, bit-exact (IEEE division, ceil/floor, same guards)
@@ -583,11 +605,7 @@ __global__ void __launch_bounds__(kOctThreads,
             const float2 cc = __ffma2_rn(fv2, __fadd2_rn(cQ, make_float2(-cP.x, -cP.y)), cP);
             x = fmaf(fw, cc.y - cc.x, cc.x);
           }
-          const float2 acc = __ffma2_rn(make_float2(x, x), make_float2(1.0f, x),
-                                        make_float2(px, pxx));
-          px = acc.x;
-          pxx = acc.y;
-          pyx = fmaf(yf, x, pyx);
+          acc_voxel(x, yf, px, pxx, pyx);
           cu += kLanes * du;
           cv += kLanes * dv;
           cw += kLanes * dw;
@@ -600,11 +618,7 @@ __global__ void __launch_bounds__(kOctThreads,
           const unsigned sel = ((unsigned)cu >> 31) | (((unsigned)cv >> 31) << 1);
           const unsigned wd = ((unsigned)cw >> 31) ? c8.y : c8.x;
           const float x = (float)__byte_perm(wd, 0u, 0x4440u | sel);
-          const float2 acc = __ffma2_rn(make_float2(x, x), make_float2(1.0f, x),
-                                        make_float2(px, pxx));
-          px = acc.x;
-          pxx = acc.y;
-          pyx = fmaf(yf, x, pyx);
+          acc_voxel(x, yf, px, pxx, pyx);
         } else if (LERP == ER_LERP_F32) {
 #if ER_OCT_FMUL2
           const float2 fuv = __fmul2_rn(make_float2(__uint2float_rz((unsigned)cu),
@@ -631,12 +645,7 @@ __global__ void __launch_bounds__(kOctThreads,
           const float2 c = __ffma2_rn(fv2, __fadd2_rn(cQ, make_float2(-cP.x, -cP.y)),
                                       cP);                      // (c0, c1)
           const float x = fmaf(fw, c.y - c.x, c.x);
-          // (sum x, sum x^2) in one packed FMA
-          const float2 acc = __ffma2_rn(make_float2(x, x), make_float2(1.0f, x),
-                                        make_float2(px, pxx));
-          px = acc.x;
-          pxx = acc.y;
-          pyx = fmaf(yf, x, pyx);
+          acc_voxel(x, yf, px, pxx, pyx);
         } else {
           const double fu = F::frac64(cu), fv = F::frac64(cv), fw = F::frac64(cw);
           // 2^52 + byte doubles: their differences are the exact byte
