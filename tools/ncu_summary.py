@@ -62,6 +62,12 @@ def report(path):
         if key in hdr:
             i = hdr.index(key)
             res[key] = [vals[i], units[i]]
+    # per-pipe utilisation (which execution pipe, if any, is the limiter)
+    for i, key in enumerate(hdr):
+        if (key.startswith("sm__inst_executed_pipe_") and key.endswith(".avg.pct_of_peak_sustained_active")) \
+                or key in ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+                           "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"):
+            res[key] = [vals[i], units[i]]
     print(json.dumps(res, indent=1))
 
 
