@@ -257,7 +257,7 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def load_traffic():
@@ -410,7 +410,7 @@ def run_ours(args):
             "precision_modes": modes,
             "gpu_launches": launches,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if launched:
         torch.distributed.destroy_process_group()
 
@@ -537,7 +537,28 @@ def run_e2e(args, t, s, ex, dev, world):
             + list(est.to_array()[3:])}
 
 
+_RESULT_OUT = None
+
+
+def emit(line: dict):
+    """The one JSON line of the contract, on the process's real stdout."""
+    out = _RESULT_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
+def _private_stdout():
+    """Keep the real stdout for the result line only and point fd 1 at stderr,
+    so banners that libraries write straight to fd 1 (NCCL prints its version
+    at communicator init) cannot add lines to the contract's output."""
+    global _RESULT_OUT
+    sys.stdout.flush()
+    _RESULT_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
 def main():
+    _private_stdout()
     args = parse()
     if args.impl == "reference":
         run_reference(args)
