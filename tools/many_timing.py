@@ -8,7 +8,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2504_19930_b200 import (Executor, PhantomSpec, RigidParams, SmcConfig, make_pair,  # noqa: E402
+from paper_2504_19930_b200 import (PhantomSpec, RigidParams, SmcConfig, make_pair,  # noqa: E402
                                    make_phantom, register_smc, register_smc_many)
 
 truth = RigidParams(math.radians(5), math.radians(-8), math.radians(4), 6.0, -4.0, 3.0)
