@@ -86,7 +86,9 @@ ER_HD void er_philox4x64_10(const uint64_t in[4], const uint64_t key_in[2], uint
   const uint64_t W0 = 0x9E3779B97F4A7C15ULL, W1 = 0xBB67AE8584CAA73BULL;
   uint64_t c0 = in[0], c1 = in[1], c2 = in[2], c3 = in[3];
   uint64_t k0 = key_in[0], k1 = key_in[1];
+#ifdef __CUDA_ARCH__
 #pragma unroll
+#endif
   for (int r = 0; r < 10; ++r) {
     if (r) {
       k0 += W0;
