@@ -36,6 +36,7 @@
 //   ER_OCT_SMEM_ACC=1      per-lane fp64 group accumulators in shared memory
 //   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2
 //   ER_OCT_ACC2=1          px += x; (pxx, pyx) by one FFMA2 of x * (x, y)
+//   ER_BITS_EXACT=1        binary sources: integer counts + fp64 boundary cells
 //                          (0: (px, pxx) by FFMA2 of x * (1, x), 2 more SASS)
 //   ER_FRAC_I2F=1          fractions by I2F on the fixed-point low word
 //   ER_OCT_TILE_MAJOR=1    tile-major CTA order (0: particle-major)
@@ -118,6 +119,11 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 // one FFMA2 whose operand pair is two computed values, no 1.0f constant)
 #ifndef ER_OCT_ACC2
 #define ER_OCT_ACC2 1
+#endif
+// bit-oct (binary source) path: uniform cells as exact integer counts, boundary
+// cells in fp64 (0: fp32 lerps and fp32 row partials like the byte path)
+#ifndef ER_BITS_EXACT
+#define ER_BITS_EXACT 1
 #endif
 
 // per-voxel fp32 row partials: sum x, sum x^2, sum y*x (both forms round identically)
@@ -535,6 +541,9 @@ __global__ void __launch_bounds__(kOctThreads,
     TgtAcc<TT> ty;
     float px = 0.f, pxx = 0.f, pyx = 0.f;
     double qx = 0.0, qxx = 0.0, qyx = 0.0;
+    // bit-oct exact path: voxels sampling exactly 1, and their target sum (u8 targets)
+    unsigned ones = 0u, ones_y = 0u;
+    constexpr bool kU8Tgt = sizeof(TT) == 1;
     constexpr bool kSmemAcc = ER_OCT_SMEM_ACC && (kF32 || BITS);
     if (kSmemAcc) racc[threadIdx.x] = make_double3(0.0, 0.0, 0.0);
     // row start in fixed point (per lane: its own row)
@@ -582,15 +591,49 @@ __global__ void __launch_bounds__(kOctThreads,
         // 32-bit cell index: the padded grid has < 2^31 cells
         const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
         if (BITS) {
-          // binary source: one byte = the cell's 8 corner bits; uniform cells
-          // (all 0 / all 1) are exact without interpolation
+          // binary source: one byte = the cell's 8 corner bits
           const unsigned c = __ldg(reinterpret_cast<const uint8_t*>(oct) +
                                    (unsigned)er_idx(cell, ncells));
-          const float yf = ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
-          float x = (c == 0xFFu) ? 1.0f : 0.0f;
+          const TT yv = __ldg(tgt + er_idx(trow - tgt + k, ntv));
+          const float yf = ty.add(yv);
+#if ER_BITS_EXACT
+          // uniform cells (all 0 / all 1) sample exactly 0 / 1: their terms are
+          // integer counts; the rare boundary cells interpolate in fp64 with
+          // the exact 32-bit fractions of the fixed-point coordinates
+          bool one = c == 0xFFu;
           if (LERP == ER_LERP_NEAREST) {
             // corner bit: u -> bit 0, v -> bit 1, w -> bit 2 (bit b = byte b of
             // the oct word); fraction >= 0.5 <=> bit 31 of the fixed-point word
+            const unsigned b = ((unsigned)cu >> 31) | (((unsigned)cv >> 31) << 1) |
+                               (((unsigned)cw >> 31) << 2);
+            one = (c >> b) & 1u;
+          } else if (c != 0u && !one) {
+            const double fu = F::frac64(cu), fv = F::frac64(cv), fw = F::frac64(cw);
+            // u-lerp of two 0/1 corners: 0, fu, 1 - fu (exact for a 32-bit
+            // fraction) or 1 -- the values fma(fu, b1 - b0, b0) takes, by selects
+            const double gu = 1.0 - fu;
+            auto pair = [c, fu, gu](int b) {
+              const unsigned lo = (c >> b) & 1u, hi = (c >> (b + 1)) & 1u;
+              return lo ? (hi ? 1.0 : gu) : (hi ? fu : 0.0);
+            };
+            const double c00 = pair(0), c10 = pair(2), c01 = pair(4), c11 = pair(6);
+            const double c0 = fma(fv, c10 - c00, c00);
+            const double c1 = fma(fv, c11 - c01, c01);
+            const double x = fma(fw, c1 - c0, c0);
+            double3 a = racc[threadIdx.x];
+            a.x += x;
+            a.y = fma(x, x, a.y);
+            a.z = fma((double)yf, x, a.z);
+            racc[threadIdx.x] = a;
+          }
+          if (one) {
+            ++ones;
+            if (kU8Tgt) ones_y += (unsigned)yv;
+            else pyx += yf;
+          }
+#else
+          float x = (c == 0xFFu) ? 1.0f : 0.0f;
+          if (LERP == ER_LERP_NEAREST) {
             const unsigned b = ((unsigned)cu >> 31) | (((unsigned)cv >> 31) << 1) |
                                (((unsigned)cw >> 31) << 2);
             x = (float)((c >> b) & 1u);
@@ -606,6 +649,7 @@ __global__ void __launch_bounds__(kOctThreads,
             x = fmaf(fw, cc.y - cc.x, cc.x);
           }
           acc_voxel(x, yf, px, pxx, pyx);
+#endif
           cu += kLanes * du;
           cv += kLanes * dv;
           cw += kLanes * dw;
@@ -689,6 +733,11 @@ __global__ void __launch_bounds__(kOctThreads,
       qx = a.x;
       qxx = a.y;
       qyx = a.z;
+    }
+    if (BITS && ER_BITS_EXACT) {  // exact integer terms of the uniform-1 voxels
+      qx += (double)ones;
+      qxx += (double)ones;
+      qyx += (double)ones_y;
     }
     // fold the group: fixed-order warp reduction in fp64 into the group slot
     double v[5];
