@@ -39,6 +39,7 @@
 //   ER_BITS_EXACT=1        binary sources: integer counts + fp64 boundary cells
 //                          (0: (px, pxx) by FFMA2 of x * (1, x), 2 more SASS)
 //   ER_FRAC_I2F=1          fractions by I2F on the fixed-point low word
+//   ER_FRAC_RN=1           ... rounded to nearest (0: truncated, biased low)
 //   ER_OCT_TILE_MAJOR=1    tile-major CTA order (0: particle-major)
 //   ER_OCT_UNROLL=1        voxel-loop unroll; ER_OCT_LDPOLICY=0 (.nc; 1 .cg, 2 .cs)
 //   ER_OCT_THREADS=256     CTA size; ER_MIN_TILES=8 minimum tiles per particle
@@ -119,6 +120,16 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 // one FFMA2 whose operand pair is two computed values, no 1.0f constant)
 #ifndef ER_OCT_ACC2
 #define ER_OCT_ACC2 1
+#endif
+// fractions from the Q32.32 low word: round to nearest (0: truncate; 7 of 32
+// full-scale image runs left the reference-order trajectory vs 3 of 32)
+#ifndef ER_FRAC_RN
+#define ER_FRAC_RN 1
+#endif
+#if ER_FRAC_RN
+#define ER_U2F __uint2float_rn
+#else
+#define ER_U2F __uint2float_rz
 #endif
 // bit-oct (binary source) path: uniform cells as exact integer counts, boundary
 // cells in fp64 (0: fp32 lerps and fp32 row partials like the byte path)
@@ -404,7 +415,7 @@ struct Fix {
   __device__ __forceinline__ static int ipart(long long q) { return (int)(q >> FB); }
   __device__ __forceinline__ static float frac32(long long q) {
 #if ER_FRAC_I2F
-    if (FB == 32) return __uint2float_rz((unsigned)q) * 2.3283064365386963e-10f;  // 2^-32
+    if (FB == 32) return ER_U2F((unsigned)q) * 2.3283064365386963e-10f;  // 2^-32
 #endif
     // top 23 fraction bits -> [1, 2) - 1
     const unsigned m = (unsigned)((unsigned long long)q >> (FB - 23)) & 0x7FFFFFu;
@@ -665,8 +676,8 @@ __global__ void __launch_bounds__(kOctThreads,
           acc_voxel(x, yf, px, pxx, pyx);
         } else if (LERP == ER_LERP_F32) {
 #if ER_OCT_FMUL2
-          const float2 fuv = __fmul2_rn(make_float2(__uint2float_rz((unsigned)cu),
-                                                    __uint2float_rz((unsigned)cv)),
+          const float2 fuv = __fmul2_rn(make_float2(ER_U2F((unsigned)cu),
+                                                    ER_U2F((unsigned)cv)),
                                         make_float2(2.3283064365386963e-10f,
                                                     2.3283064365386963e-10f));
           const float fu = fuv.x, fv = fuv.y, fw = F::frac32(cw);
