@@ -6,7 +6,7 @@ stands in for the reference here: for seeds 0..N-1 run C2 (image, 2000 x 50)
 and a C3-style mask registration (2000 x 50 on the 176x176x208 masks) in
 f32 / f64 / exact and report the final-transform differences.
 
-    python tools/seed_study.py [n_seeds] [image,mask]"""
+    python tools/seed_study.py [n_seeds] [image,mask] [first_seed]"""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -15,6 +15,7 @@ from paper_2504_19930_b200 import Executor, SmcConfig, binarize, register_smc
 
 n_seeds = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["image", "mask"]
+first = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 t, s, case = bench.make_workload()
 tm, sm = binarize(case.target_masks[0], 0.5), binarize(case.source_masks[0], 0.5)
 sp = np.asarray(t.spacing)
@@ -22,7 +23,7 @@ for mode, (a, b) in (("image", (t, s)), ("mask", (tm, sm))):
     if mode not in modes:
         continue
     rows = []
-    for seed in range(n_seeds):
+    for seed in range(first, first + n_seeds):
         cfg = SmcConfig(mode=mode, n_particles=2000, n_iterations=50, seed=seed)
         res = {}
         for prec in ("exact", "f64", "f32"):
