@@ -32,7 +32,8 @@
 // scripts tools/variants*.sh and are recorded in profiles/README.md):
 //   ER_OCT_HALF=1          two rows per warp on 16-lane halves (0: one row, 32 lanes)
 //   ER_OCT_MINBLOCKS_F32=5 CTAs/SM for the fp32-class oct kernels (4: 62 regs; 6 spills)
-//   ER_OCT_MINBLOCKS_F64=3 CTAs/SM for the fp64-lerp oct kernel
+//   ER_OCT_MINBLOCKS_F64=6 CTAs/SM for the fp64-lerp oct kernel (128 threads each)
+//   ER_OCT_THREADS_F64=128 CTA size of the fp64-lerp oct kernel
 //   ER_OCT_SMEM_ACC=1      per-lane fp64 group accumulators in shared memory
 //   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2
 //   ER_OCT_ACC2=1          px += x; (pxx, pyx) by one FFMA2 of x * (x, y)
@@ -64,8 +65,16 @@ constexpr int kThreads = 256;
 #ifndef ER_OCT_THREADS
 #define ER_OCT_THREADS 256
 #endif
-constexpr int kOctThreads = ER_OCT_THREADS;  // oct fast path CTA size
-constexpr int kOctWarps = kOctThreads / 32;
+// fp64-lerp oct kernel: 128-thread CTAs, 6 per SM (+3.3% over 256 x 3 on C2)
+#ifndef ER_OCT_THREADS_F64
+#define ER_OCT_THREADS_F64 128
+#endif
+// oct fast path CTA size per sampling mode
+template <int LERP>
+struct OctThreads {
+  static constexpr int n = LERP == ER_LERP_F64 ? ER_OCT_THREADS_F64 : ER_OCT_THREADS;
+  static constexpr int warps = n / 32;
+};
 constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerTile = 2048;
 
@@ -102,7 +111,7 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 #define ER_OCT_MINBLOCKS_F32 5
 #endif
 #ifndef ER_OCT_MINBLOCKS_F64
-#define ER_OCT_MINBLOCKS_F64 3
+#define ER_OCT_MINBLOCKS_F64 (3 * 256 / ER_OCT_THREADS_F64)
 #endif
 #ifndef ER_MIN_TILES
 #define ER_MIN_TILES 8
@@ -474,7 +483,7 @@ struct OctGeom {
 // BITS = 1: `oct` points at the bit-oct layout of a binary source (1 byte per
 // cell) and the lerps run in fp32 (row partials folded per row as below).
 template <typename TT, int LERP, int BITS = 0>
-__global__ void __launch_bounds__(kOctThreads,
+__global__ void __launch_bounds__(OctThreads<LERP>::n,
                                    LERP != ER_LERP_F64 ? ER_OCT_MINBLOCKS_F32 : ER_OCT_MINBLOCKS_F64)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
@@ -522,6 +531,8 @@ __global__ void __launch_bounds__(kOctThreads,
   // the result does not depend on which warp ran which group.
   __shared__ double gsum[kRowsPerTile / 32][5];
   __shared__ int next_group;
+  constexpr int kOctThreads = OctThreads<LERP>::n;
+  constexpr int kOctWarps = OctThreads<LERP>::warps;
   __shared__ RowRec rrec[kOctWarps][32];
   __shared__ double3 racc[ER_OCT_SMEM_ACC ? kOctThreads : 1];
   const int ngroups = (R + 31) / 32;  // <= kRowsPerTile / 32 (make_geom)
@@ -1005,7 +1016,7 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
     const unsigned blocks = (unsigned)(P * g.ntiles);
     const uint2* lay = (const uint2*)(use_bits ? src->bitoct_dev : src->oct_dev);
 #define ER_OCT(TT, L, B) \
-  measure_oct_kernel<TT, L, B><<<blocks, kOctThreads, 0, st>>>((const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part)
+  measure_oct_kernel<TT, L, B><<<blocks, OctThreads<L>::n, 0, st>>>((const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part)
 #define ER_OCT_BITS(TT)                                                   \
   do {                                                                    \
     if (lerp_mode == ER_LERP_NEAREST) ER_OCT(TT, ER_LERP_NEAREST, 1);     \
