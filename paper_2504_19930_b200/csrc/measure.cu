@@ -45,6 +45,8 @@
 //   ER_OCT_UNROLL=1        voxel-loop unroll; ER_OCT_LDPOLICY=0 (.nc; 1 .cg, 2 .cs)
 //   ER_OCT_THREADS=256     CTA size; ER_MIN_TILES=8 minimum tiles per particle
 //   ER_BOUNDS_CHECK=0      debug build: every gather index range-checked (common.cuh)
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace {
@@ -63,7 +65,7 @@ struct Geom {
 
 constexpr int kThreads = 256;
 #ifndef ER_OCT_THREADS
-#define ER_OCT_THREADS 256
+#define ER_OCT_THREADS 128
 #endif
 // fp64-lerp oct kernel: 128-thread CTAs, 6 per SM (+3.3% over 256 x 3 on C2)
 #ifndef ER_OCT_THREADS_F64
@@ -80,6 +82,19 @@ constexpr int kRowsPerTile = 2048;
 
 #ifndef ER_OCT_HALF
 #define ER_OCT_HALF 1
+#endif
+// lanes per target row in the oct kernels (8, 16 or 32; rows per warp = 32 / lanes)
+#ifndef ER_OCT_LANES
+#define ER_OCT_LANES (ER_OCT_HALF ? 8 : 32)
+#endif
+// 8-bit target values to float on the XU pipe (I2F.U8) instead of the ALU (I2FP)
+#ifndef ER_TGT_XU
+#define ER_TGT_XU 1
+#endif
+
+// fp32 byte path: two voxels per lane per step, lerps packed across them
+#ifndef ER_OCT_PAIR
+#define ER_OCT_PAIR 1
 #endif
 #ifndef ER_OCT_UNROLL
 #define ER_OCT_UNROLL 1
@@ -108,7 +123,7 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 #define ER_UNROLL_(n) ER_PRAGMA_(unroll n)
 #define ER_UNROLL(n) ER_UNROLL_(n)
 #ifndef ER_OCT_MINBLOCKS_F32
-#define ER_OCT_MINBLOCKS_F32 5
+#define ER_OCT_MINBLOCKS_F32 9
 #endif
 #ifndef ER_OCT_MINBLOCKS_F64
 #define ER_OCT_MINBLOCKS_F64 (3 * 256 / ER_OCT_THREADS_F64)
@@ -436,16 +451,25 @@ struct Fix {
   }
 };
 
-template <typename TT>
-struct TgtAcc;  // per-row accumulation of target terms
-
-template <>
-struct TgtAcc<uint8_t> {  // exact integer sums of an 8-bit target
-  unsigned y = 0, yy = 0;
-  __device__ __forceinline__ float add(uint8_t v) {
-    y += v;
-    yy += (unsigned)v * v;
-    return (float)v;
+// Per-lane accumulation of the target terms sum y (and sum y^2, which only the
+// overlap region needs: the full region takes the target totals from the
+// precomputed moments, kernels_numba.py:172-177 -- OVL = 0 drops it).
+//   * 8-bit targets: exact integer sums, folded into fp64 once per 32-row group;
+//     the value handed to the y*x product is the exact byte as a float.
+//   * fp32/fp64-stored targets in the fp32-class modes: fp32 row partials, folded
+//     into fp64 at every row end (kRowFold), like the source partials.
+//   * fp32/fp64-stored targets in the fp64-lerp mode: fp64 throughout, and the
+//     y*x product sees the unrounded stored value.
+template <typename TT, int LERP, int OVL>
+struct TgtAcc {
+  using V = typename std::conditional<LERP == ER_LERP_F64, double, float>::type;
+  static constexpr bool kRowFold = LERP != ER_LERP_F64;
+  V y = 0, yy = 0;
+  __device__ __forceinline__ V add(TT v) {
+    const V f = (V)v;
+    y += f;
+    if (OVL) yy = fma(f, f, yy);
+    return f;
   }
   __device__ __forceinline__ void fold(double& sy, double& syy) {
     sy += (double)y;
@@ -454,21 +478,93 @@ struct TgtAcc<uint8_t> {  // exact integer sums of an 8-bit target
   }
 };
 
-template <typename TT>
-struct TgtAcc {
-  float y = 0.f, yy = 0.f;
-  __device__ __forceinline__ float add(TT v) {
-    const float f = (float)v;
-    y += f;
-    yy = fmaf(f, f, yy);
-    return f;
+template <int LERP, int OVL>
+struct TgtAcc<uint8_t, LERP, OVL> {
+  using V = float;
+  static constexpr bool kRowFold = false;
+  unsigned y = 0, yy = 0;
+  __device__ __forceinline__ float add(uint8_t v) {
+    y += v;
+    if (OVL) yy += (unsigned)v * v;
+    return __uint2float_rn(v);
+  }
+  // two voxels at once (one 3-input add)
+  __device__ __forceinline__ float2 add2(uint8_t a, uint8_t b) {
+    y += (unsigned)a + (unsigned)b;
+    if (OVL) yy += (unsigned)a * a + (unsigned)b * b;
+    return make_float2(u8f(a), u8f(b));
+  }
+  __device__ __forceinline__ static float u8f(uint8_t v) {
+#if ER_TGT_XU
+    float r;
+    asm("cvt.rn.f32.u8 %0, %1;" : "=f"(r) : "h"((unsigned short)v));
+    return r;
+#else
+    return __uint2float_rn(v);
+#endif
   }
   __device__ __forceinline__ void fold(double& sy, double& syy) {
     sy += (double)y;
     syy += (double)yy;
-    y = yy = 0.f;
+    y = yy = 0;
   }
 };
+
+template <typename TT, int LERP, int OVL>
+__device__ __forceinline__ float2 tgt_add2(TgtAcc<TT, LERP, OVL>& t, TT a, TT b) {
+  const float fa = (float)t.add(a);
+  const float fb = (float)t.add(b);
+  return make_float2(fa, fb);
+}
+template <int LERP, int OVL>
+__device__ __forceinline__ float2 tgt_add2(TgtAcc<uint8_t, LERP, OVL>& t, uint8_t a, uint8_t b) {
+  return t.add2(a, b);
+}
+
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+
+// fp32 trilinear sample of one oct cell (8 corner bytes), packed fp32x2:
+// corners paired along k so the u-lerps yield (c00, c01) and (c10, c11) and the
+// v-lerp runs packed too.  2^23-offset floats: their differences are exact, and
+// so is removing the offset.
+__device__ __forceinline__ float lerp_oct_f32(uint2 c8, float fu, float fv, float fw) {
+  const float2 P0 = make_float2(byte_magic(c8.x, 0), byte_magic(c8.y, 0));
+  const float2 P1 = make_float2(byte_magic(c8.x, 1), byte_magic(c8.y, 1));
+  const float2 Q0 = make_float2(byte_magic(c8.x, 2), byte_magic(c8.y, 2));
+  const float2 Q1 = make_float2(byte_magic(c8.x, 3), byte_magic(c8.y, 3));
+  const float2 off2 = make_float2(-8388608.0f, -8388608.0f);
+  const float2 fu2 = make_float2(fu, fu), fv2 = make_float2(fv, fv);
+  const float2 cP = __ffma2_rn(fu2, f2sub(P1, P0), __fadd2_rn(P0, off2));  // (c00, c01)
+  const float2 cQ = __ffma2_rn(fu2, f2sub(Q1, Q0), __fadd2_rn(Q0, off2));  // (c10, c11)
+  const float2 c = __ffma2_rn(fv2, f2sub(cQ, cP), cP);                      // (c0, c1)
+  return fmaf(fw, c.y - c.x, c.x);
+}
+
+// The same sample for two voxels a, b at once, packed ACROSS the voxels: every
+// lerp of the chain (u, v and w) is one FFMA2, the fractions arrive as pairs,
+// and the per-element operations are exactly those of lerp_oct_f32, so each
+// sample is bit-identical to the single-voxel form.
+__device__ __forceinline__ float2 lerp_oct_f32x2(uint2 a8, uint2 b8, float2 fu, float2 fv,
+                                                 float2 fw) {
+  const float2 off2 = make_float2(-8388608.0f, -8388608.0f);
+  const float2 x000 = make_float2(byte_magic(a8.x, 0), byte_magic(b8.x, 0));
+  const float2 x100 = make_float2(byte_magic(a8.x, 1), byte_magic(b8.x, 1));
+  const float2 x010 = make_float2(byte_magic(a8.x, 2), byte_magic(b8.x, 2));
+  const float2 x110 = make_float2(byte_magic(a8.x, 3), byte_magic(b8.x, 3));
+  const float2 x001 = make_float2(byte_magic(a8.y, 0), byte_magic(b8.y, 0));
+  const float2 x101 = make_float2(byte_magic(a8.y, 1), byte_magic(b8.y, 1));
+  const float2 x011 = make_float2(byte_magic(a8.y, 2), byte_magic(b8.y, 2));
+  const float2 x111 = make_float2(byte_magic(a8.y, 3), byte_magic(b8.y, 3));
+  const float2 c00 = __ffma2_rn(fu, f2sub(x100, x000), __fadd2_rn(x000, off2));
+  const float2 c10 = __ffma2_rn(fu, f2sub(x110, x010), __fadd2_rn(x010, off2));
+  const float2 c01 = __ffma2_rn(fu, f2sub(x101, x001), __fadd2_rn(x001, off2));
+  const float2 c11 = __ffma2_rn(fu, f2sub(x111, x011), __fadd2_rn(x011, off2));
+  const float2 c0 = __ffma2_rn(fv, f2sub(c10, c00), c00);
+  const float2 c1 = __ffma2_rn(fv, f2sub(c11, c01), c01);
+  return __ffma2_rn(fw, f2sub(c1, c0), c0);
+}
 
 struct RowRec {  // one target row of a 32-row group, in fixed point
   long long fu0, fv0, fw0;
@@ -480,9 +576,11 @@ struct OctGeom {
   long long P; // particles in the launch (tile-major block order)
 };
 
+
 // BITS = 1: `oct` points at the bit-oct layout of a binary source (1 byte per
-// cell) and the lerps run in fp32 (row partials folded per row as below).
-template <typename TT, int LERP, int BITS = 0>
+// cell).  OVL = 1: the overlap region (sum y^2 over the in-bounds voxels is
+// accumulated; the full region takes it from the target moments).
+template <typename TT, int LERP, int BITS, int OVL>
 __global__ void __launch_bounds__(OctThreads<LERP>::n,
                                    LERP != ER_LERP_F64 ? ER_OCT_MINBLOCKS_F32 : ER_OCT_MINBLOCKS_F64)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
@@ -491,6 +589,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   // fp32-class modes (fp32 lerps, nearest) use Q32.32 coordinates and fp32 row partials
   constexpr bool kF32 = LERP != ER_LERP_F64;
   using F = Fix<kF32 ? 32 : 40>;
+  using Acc = TgtAcc<TT, LERP, OVL>;
 #if ER_OCT_TILE_MAJOR
   // tile-major launch order: the CTAs resident at any moment work on the same
   // target slab for many particles, so the union of their source footprints
@@ -533,12 +632,26 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   __shared__ int next_group;
   constexpr int kOctThreads = OctThreads<LERP>::n;
   constexpr int kOctWarps = OctThreads<LERP>::warps;
+  constexpr bool kSmemAcc = ER_OCT_SMEM_ACC && (kF32 || BITS);
+  constexpr bool kTgtRowFold = Acc::kRowFold && (kF32 || BITS);
   __shared__ RowRec rrec[kOctWarps][32];
-  __shared__ double3 racc[ER_OCT_SMEM_ACC ? kOctThreads : 1];
+  __shared__ double3 racc[kSmemAcc ? kOctThreads : 1];
+  // fp64 row folds of the target terms of fp32/fp64-stored targets
+  __shared__ double2 tacc[kTgtRowFold ? kOctThreads : 1];
   const int ngroups = (R + 31) / 32;  // <= kRowsPerTile / 32 (make_geom)
   if (threadIdx.x == 0) next_group = kOctWarps;
   __syncthreads();
   int cnt = 0;
+  // kLanes lanes per row: 32 (one row at a time) or 16 (two rows side by
+  // side on the half-warps: for nz = 208 = 13 x 16 no lane idles at the row
+  // end, and each lane's per-row overhead is paid over twice the voxels)
+  constexpr int kLanes = ER_OCT_LANES;
+  constexpr int kRowsPerWarp = 32 / kLanes;
+  const int sub = lane & (kLanes - 1);
+  // fp32 byte path: voxels k and k + kLanes of a lane are sampled together
+  constexpr bool kPair = ER_OCT_PAIR && LERP == ER_LERP_F32 && !BITS;
+  const long long du1 = kLanes * du, dv1 = kLanes * dv, dw1 = kLanes * dw;
+  const long long du2 = 2 * du1, dv2 = 2 * dv1, dw2 = 2 * dw1;
 
   for (int grp = warp; grp < ngroups;) {
     const int r = grp * 32 + lane;
@@ -560,14 +673,14 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
     }
     cnt += khi - klo;
     // per-lane group partials: fp32 (LERP_F32) or fp64, exact ints for u8 targets
-    TgtAcc<TT> ty;
+    Acc ty;
     float px = 0.f, pxx = 0.f, pyx = 0.f;
     double qx = 0.0, qxx = 0.0, qyx = 0.0;
     // bit-oct exact path: voxels sampling exactly 1, and their target sum (u8 targets)
     unsigned ones = 0u, ones_y = 0u;
     constexpr bool kU8Tgt = sizeof(TT) == 1;
-    constexpr bool kSmemAcc = ER_OCT_SMEM_ACC && (kF32 || BITS);
     if (kSmemAcc) racc[threadIdx.x] = make_double3(0.0, 0.0, 0.0);
+    if (kTgtRowFold) tacc[threadIdx.x] = make_double2(0.0, 0.0);
     // row start in fixed point (per lane: its own row)
     // (the +1.0 voxel shift to the padded cell index is an exact integer add,
     // so the cell index below is a plain non-negative 32-bit IMAD chain)
@@ -583,41 +696,83 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
     mine.off = off;
     unsigned rows = __ballot_sync(0xffffffffu, khi > klo);
     __syncwarp();
-    // kLanes lanes per row: 32 (one row at a time) or 16 (two rows side by
-    // side on the half-warps: for nz = 208 = 13 x 16 no lane idles at the row
-    // end, and each lane's per-row overhead is paid over twice the voxels)
-    constexpr int kLanes = ER_OCT_HALF ? 16 : 32;
-    const int sub = lane & (kLanes - 1);
     while (rows) {
-      int q = __ffs(rows) - 1;
-      rows &= rows - 1;
-      if (kLanes == 16) {
-        const int q2 = rows ? __ffs(rows) - 1 : -1;
-        if (q2 >= 0) rows &= rows - 1;
-        if (lane >= 16) q = q2;
+      // the next kRowsPerWarp non-empty rows, one per lane group (uniform)
+      int q = -1;
+      const int myslot = lane / kLanes;
+#pragma unroll
+      for (int s = 0; s < kRowsPerWarp; ++s) {
+        const int b = rows ? __ffs(rows) - 1 : -1;
+        if (b >= 0) rows &= rows - 1;
+        if (s == myslot) q = b;
       }
-      int qhi = 0, k0 = 1;
-      const TT* __restrict__ trow = tgt;
+      int qhi = 0, k0 = 1, toff = 0;
       long long cu = 0, cv = 0, cw = 0;
       if (q >= 0) {
         const RowRec& rq = rrec[warp][q];
         qhi = rq.khi;
         k0 = rq.klo + sub;
-        trow = tgt + rq.off;
+        toff = rq.off;
         cu = rq.fu0 + (long long)k0 * du;
         cv = rq.fv0 + (long long)k0 * dv;
         cw = rq.fw0 + (long long)k0 * dw;
       }
+      int k = k0;
+      if (kPair) {
+        // two voxels per lane per step (k and k + kLanes): the fractions, the
+        // whole lerp chain and the accumulation run as fp32x2 pairs across the
+        // two voxels; the loop control, the target row address and the
+        // target sum are shared
+        float2 sx2 = make_float2(0.f, 0.f), sxx2 = sx2, syx2 = sx2;
+        const float s32 = 2.3283064365386963e-10f;  // 2^-32
+        // voxel b = voxel a + kLanes along the row: its own coordinate set,
+        // both stepped by 2 kLanes per iteration
+        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
+        // loop on the target index (toff + k): one induction variable for the
+        // loop test and the target address
+        int ti = toff + k;
+        const int ti_end = toff + qhi - kLanes;
+        for (; ti < ti_end; ti += 2 * kLanes) {
+          // Horner form: two IMADs per cell index
+          const int ca = (F::ipart(cu) * og.cy + F::ipart(cv)) * og.cz + F::ipart(cw);
+          const int cb = (F::ipart(bu) * og.cy + F::ipart(bv)) * og.cz + F::ipart(bw);
+          const uint2 a8 = ld_oct(oct + (unsigned)er_idx(ca, ncells));
+          const uint2 b8 = ld_oct(oct + (unsigned)er_idx(cb, ncells));
+          const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
+          const TT ya = __ldg(tp);
+          const TT yb = __ldg(tp + kLanes);
+          const float2 y2 = tgt_add2(ty, ya, yb);
+          const float2 sc = make_float2(s32, s32);
+          const float2 fu = __fmul2_rn(make_float2(ER_U2F((unsigned)cu), ER_U2F((unsigned)bu)), sc);
+          const float2 fv = __fmul2_rn(make_float2(ER_U2F((unsigned)cv), ER_U2F((unsigned)bv)), sc);
+          const float2 fw = __fmul2_rn(make_float2(ER_U2F((unsigned)cw), ER_U2F((unsigned)bw)), sc);
+          const float2 x = lerp_oct_f32x2(a8, b8, fu, fv, fw);
+          sx2 = __fadd2_rn(sx2, x);
+          sxx2 = __ffma2_rn(x, x, sxx2);
+          syx2 = __ffma2_rn(x, y2, syx2);
+          cu += du2;
+          cv += dv2;
+          cw += dw2;
+          bu += du2;
+          bv += dv2;
+          bw += dw2;
+        }
+        k = ti - toff;
+        px = sx2.x + sx2.y;
+        pxx = sxx2.x + sxx2.y;
+        pyx = syx2.x + syx2.y;
+      }
       ER_UNROLL(ER_OCT_UNROLL)
-      for (int k = k0; k < qhi; k += kLanes) {
+      for (; k < qhi; k += kLanes) {
         // 32-bit cell index: the padded grid has < 2^31 cells
         const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
+        const TT* tp = tgt + (unsigned)er_idx(toff + k, ntv);
         if (BITS) {
           // binary source: one byte = the cell's 8 corner bits
           const unsigned c = __ldg(reinterpret_cast<const uint8_t*>(oct) +
                                    (unsigned)er_idx(cell, ncells));
-          const TT yv = __ldg(tgt + er_idx(trow - tgt + k, ntv));
-          const float yf = ty.add(yv);
+          const TT yv = __ldg(tp);
+          const auto yf = ty.add(yv);
 #if ER_BITS_EXACT
           // uniform cells (all 0 / all 1) sample exactly 0 / 1: their terms are
           // integer counts; the rare boundary cells interpolate in fp64 with
@@ -651,7 +806,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
           if (one) {
             ++ones;
             if (kU8Tgt) ones_y += (unsigned)yv;
-            else pyx += yf;
+            else pyx += (float)yf;
           }
 #else
           float x = (c == 0xFFu) ? 1.0f : 0.0f;
@@ -665,26 +820,26 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
             const float2 P0 = make_float2(bit(0), bit(4)), P1 = make_float2(bit(1), bit(5));
             const float2 Q0 = make_float2(bit(2), bit(6)), Q1 = make_float2(bit(3), bit(7));
             const float2 fu2 = make_float2(fu, fu), fv2 = make_float2(fv, fv);
-            const float2 cP = __ffma2_rn(fu2, __fadd2_rn(P1, make_float2(-P0.x, -P0.y)), P0);
-            const float2 cQ = __ffma2_rn(fu2, __fadd2_rn(Q1, make_float2(-Q0.x, -Q0.y)), Q0);
-            const float2 cc = __ffma2_rn(fv2, __fadd2_rn(cQ, make_float2(-cP.x, -cP.y)), cP);
+            const float2 cP = __ffma2_rn(fu2, f2sub(P1, P0), P0);
+            const float2 cQ = __ffma2_rn(fu2, f2sub(Q1, Q0), Q0);
+            const float2 cc = __ffma2_rn(fv2, f2sub(cQ, cP), cP);
             x = fmaf(fw, cc.y - cc.x, cc.x);
           }
-          acc_voxel(x, yf, px, pxx, pyx);
+          acc_voxel(x, (float)yf, px, pxx, pyx);
 #endif
-          cu += kLanes * du;
-          cv += kLanes * dv;
-          cw += kLanes * dw;
+          cu += du1;
+          cv += dv1;
+          cw += dw1;
           continue;
         }
         const uint2 c8 = ld_oct(oct + (unsigned)er_idx(cell, ncells));
-        const float yf = ty.add(__ldg(tgt + er_idx(trow - tgt + k, ntv)));
+        const auto yv = ty.add(__ldg(tp));
         if (LERP == ER_LERP_NEAREST) {
           // nearest corner byte: u -> byte bit 0, v -> byte bit 1, w -> word
           const unsigned sel = ((unsigned)cu >> 31) | (((unsigned)cv >> 31) << 1);
           const unsigned wd = ((unsigned)cw >> 31) ? c8.y : c8.x;
           const float x = (float)__byte_perm(wd, 0u, 0x4440u | sel);
-          acc_voxel(x, yf, px, pxx, pyx);
+          acc_voxel(x, (float)yv, px, pxx, pyx);
         } else if (LERP == ER_LERP_F32) {
 #if ER_OCT_FMUL2
           const float2 fuv = __fmul2_rn(make_float2(ER_U2F((unsigned)cu),
@@ -695,23 +850,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
 #else
           const float fu = F::frac32(cu), fv = F::frac32(cv), fw = F::frac32(cw);
 #endif
-          // packed fp32x2 (FFMA2/FADD2): corners paired along k so the u-lerps
-          // yield (c00, c01) and (c10, c11) and the v-lerp runs packed too
-          const float2 P0 = make_float2(byte_magic(c8.x, 0), byte_magic(c8.y, 0));
-          const float2 P1 = make_float2(byte_magic(c8.x, 1), byte_magic(c8.y, 1));
-          const float2 Q0 = make_float2(byte_magic(c8.x, 2), byte_magic(c8.y, 2));
-          const float2 Q1 = make_float2(byte_magic(c8.x, 3), byte_magic(c8.y, 3));
-          const float2 off2 = make_float2(-8388608.0f, -8388608.0f);
-          const float2 fu2 = make_float2(fu, fu), fv2 = make_float2(fv, fv);
-          // differences of the 2^23-offset floats are exact; so is removing the offset
-          const float2 cP = __ffma2_rn(fu2, __fadd2_rn(P1, make_float2(-P0.x, -P0.y)),
-                                       __fadd2_rn(P0, off2));   // (c00, c01)
-          const float2 cQ = __ffma2_rn(fu2, __fadd2_rn(Q1, make_float2(-Q0.x, -Q0.y)),
-                                       __fadd2_rn(Q0, off2));   // (c10, c11)
-          const float2 c = __ffma2_rn(fv2, __fadd2_rn(cQ, make_float2(-cP.x, -cP.y)),
-                                      cP);                      // (c0, c1)
-          const float x = fmaf(fw, c.y - c.x, c.x);
-          acc_voxel(x, yf, px, pxx, pyx);
+          acc_voxel(lerp_oct_f32(c8, fu, fv, fw), (float)yv, px, pxx, pyx);
         } else {
           const double fu = F::frac64(cu), fv = F::frac64(cv), fw = F::frac64(cw);
           // 2^52 + byte doubles: their differences are the exact byte
@@ -729,11 +868,11 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
           const double x = fma(fw, c1 - c0, c0);
           qx += x;
           qxx = fma(x, x, qxx);
-          qyx = fma((double)yf, x, qyx);
+          qyx = fma((double)yv, x, qyx);
         }
-        cu += kLanes * du;
-        cv += kLanes * dv;
-        cw += kLanes * dw;
+        cu += du1;
+        cv += dv1;
+        cw += dw1;
       }
       if (kF32 || BITS) {  // fp32 row partials (<= nz/kLanes voxels) -> fp64
         if (kSmemAcc) {
@@ -748,6 +887,11 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
           qyx += (double)pyx;
         }
         px = pxx = pyx = 0.f;
+        if (kTgtRowFold) {
+          double2 t = tacc[threadIdx.x];
+          ty.fold(t.x, t.y);
+          tacc[threadIdx.x] = t;
+        }
       }
     }
     if (kSmemAcc) {
@@ -768,7 +912,13 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
     v[2] = qyx;
     v[3] = 0.0;
     v[4] = 0.0;
-    ty.fold(v[3], v[4]);
+    if (kTgtRowFold) {
+      const double2 t = tacc[threadIdx.x];
+      v[3] = t.x;
+      v[4] = t.y;
+    } else {
+      ty.fold(v[3], v[4]);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
@@ -1015,8 +1165,15 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
     const OctGeom og{src->ny + 1, src->nz + 1, (long long)P};
     const unsigned blocks = (unsigned)(P * g.ntiles);
     const uint2* lay = (const uint2*)(use_bits ? src->bitoct_dev : src->oct_dev);
-#define ER_OCT(TT, L, B) \
-  measure_oct_kernel<TT, L, B><<<blocks, OctThreads<L>::n, 0, st>>>((const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part)
+#define ER_OCT(TT, L, B)                                                                   \
+  do {                                                                                     \
+    if (overlap_only)                                                                      \
+      measure_oct_kernel<TT, L, B, 1><<<blocks, OctThreads<L>::n, 0, st>>>(                \
+          (const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part);                       \
+    else                                                                                   \
+      measure_oct_kernel<TT, L, B, 0><<<blocks, OctThreads<L>::n, 0, st>>>(                \
+          (const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part);                       \
+  } while (0)
 #define ER_OCT_BITS(TT)                                                   \
   do {                                                                    \
     if (lerp_mode == ER_LERP_NEAREST) ER_OCT(TT, ER_LERP_NEAREST, 1);     \
