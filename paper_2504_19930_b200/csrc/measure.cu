@@ -123,7 +123,7 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 #define ER_UNROLL_(n) ER_PRAGMA_(unroll n)
 #define ER_UNROLL(n) ER_UNROLL_(n)
 #ifndef ER_OCT_MINBLOCKS_F32
-#define ER_OCT_MINBLOCKS_F32 9
+#define ER_OCT_MINBLOCKS_F32 8
 #endif
 #ifndef ER_OCT_MINBLOCKS_F64
 #define ER_OCT_MINBLOCKS_F64 (3 * 256 / ER_OCT_THREADS_F64)
@@ -725,13 +725,14 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
         // target sum are shared
         float2 sx2 = make_float2(0.f, 0.f), sxx2 = sx2, syx2 = sx2;
         const float s32 = 2.3283064365386963e-10f;  // 2^-32
-        // voxel b = voxel a + kLanes along the row: its own coordinate set,
-        // both stepped by 2 kLanes per iteration
-        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
+        const float2 sc = make_float2(s32, s32);
         // loop on the target index (toff + k): one induction variable for the
         // loop test and the target address
         int ti = toff + k;
         const int ti_end = toff + qhi - kLanes;
+        // voxel b = voxel a + kLanes along the row: its own coordinate set,
+        // both stepped by 2 kLanes per iteration
+        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
         for (; ti < ti_end; ti += 2 * kLanes) {
           // Horner form: two IMADs per cell index
           const int ca = (F::ipart(cu) * og.cy + F::ipart(cv)) * og.cz + F::ipart(cw);
@@ -742,7 +743,6 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
           const TT ya = __ldg(tp);
           const TT yb = __ldg(tp + kLanes);
           const float2 y2 = tgt_add2(ty, ya, yb);
-          const float2 sc = make_float2(s32, s32);
           const float2 fu = __fmul2_rn(make_float2(ER_U2F((unsigned)cu), ER_U2F((unsigned)bu)), sc);
           const float2 fv = __fmul2_rn(make_float2(ER_U2F((unsigned)cv), ER_U2F((unsigned)bv)), sc);
           const float2 fw = __fmul2_rn(make_float2(ER_U2F((unsigned)cw), ER_U2F((unsigned)bw)), sc);
