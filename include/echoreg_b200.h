@@ -129,7 +129,13 @@ int er_convert_f64(const double *data_dev, int64_t n, int32_t dst_dtype, void *d
  * (backend.py:78-108) dispatches to.  A_dev: P x 9 (row-major 3x3 index
  * affine, geometry.index_affine), b_dev: P x 3.  tgt_moments_dev: the
  * er_volume_moments() of the target.  Outputs: squared NCC (f64), the
- * degenerate flag, and the exact in-bounds voxel count per particle. */
+ * degenerate flag, and the exact in-bounds voxel count per particle.
+ * In ER_LERP_F32 on a non-binary source, particles whose fp32 samples
+ * cannot resolve the likelihood to 1e-4 relative (or the degenerate test)
+ * -- ill-conditioned, nearly decorrelated or nearly constant overlaps -- are
+ * re-measured on the device in ER_LERP_EXACT arithmetic before return (no
+ * host round trip; the workspace holds the list).  The workspace is
+ * P x tiles x 48 B of partials + 16 B + 4 B per particle. */
 size_t er_measure_workspace_bytes(const er_volume *tgt, int64_t P);
 int er_measure_ncc(const er_volume *tgt, const er_volume *src, const double *tgt_moments_dev,
                    const double *A_dev, const double *b_dev, int64_t P, int32_t overlap_only,

@@ -83,6 +83,10 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_OCT_HALF
 #define ER_OCT_HALF 1
 #endif
+// fp32-lerp measurements: re-measure ill-conditioned particles in fp64 (RefineArgs)
+#ifndef ER_REFINE
+#define ER_REFINE 1
+#endif
 // lanes per target row in the oct kernels (8, 16 or 32; rows per warp = 32 / lanes)
 #ifndef ER_OCT_LANES
 #define ER_OCT_LANES (ER_OCT_HALF ? 8 : 32)
@@ -329,17 +333,19 @@ __device__ __forceinline__ void block_write_partial(double sx, double sxx, doubl
       out.yy += red[w][4];
       out.n += redn[w];
     }
-    part[blockIdx.x] = out;
+    *part = out;
   }
 }
 
+// One (particle, tile) of the generic kernel: sums over the tile's rows into
+// part[slot].  Ends with the block reduction (its __syncthreads makes it safe
+// to call repeatedly from one CTA).
 template <typename TT, typename ST, int LERP>
-__global__ void __launch_bounds__(kThreads, 3)
-    measure_partials_kernel(const TT* __restrict__ tgt, const ST* __restrict__ src,
-                            const double* __restrict__ A, const double* __restrict__ B,
-                            const Geom g, Partial* __restrict__ part) {
-  const int tile = blockIdx.x % g.ntiles;
-  const long long p = blockIdx.x / g.ntiles;
+__device__ __forceinline__ void partials_cta(const TT* __restrict__ tgt,
+                                             const ST* __restrict__ src,
+                                             const double* __restrict__ A,
+                                             const double* __restrict__ B, const Geom& g,
+                                             long long p, int tile, Partial* __restrict__ part) {
   const double* Ap = A + 9 * p;
   const double* Bp = B + 3 * p;
   const double a00 = Ap[0], a01 = Ap[1], a02 = Ap[2];
@@ -404,6 +410,38 @@ __global__ void __launch_bounds__(kThreads, 3)
   }
 
   block_write_partial(sx, sxx, syx, sy, syy, cnt, part);
+}
+
+template <typename TT, typename ST, int LERP>
+__global__ void __launch_bounds__(kThreads, 3)
+    measure_partials_kernel(const TT* __restrict__ tgt, const ST* __restrict__ src,
+                            const double* __restrict__ A, const double* __restrict__ B,
+                            const Geom g, Partial* __restrict__ part) {
+  const int tile = blockIdx.x % g.ntiles;
+  const long long p = blockIdx.x / g.ntiles;
+  partials_cta<TT, ST, LERP>(tgt, src, A, B, g, p, tile, part + blockIdx.x);
+}
+
+// Refinement pass: the particles the fp32 finalize listed as ill-conditioned
+// (list[0 .. *count)) re-measured with the reference-order fp64 arithmetic
+// (LERP_EXACT) on the plain copy of the source; a fixed persistent grid walks
+// the (particle, tile) items, so nothing is launched per particle and an
+// empty list costs one pass of idle CTAs.  Each item overwrites that
+// particle's own partial slots (fixed tiling -> the sums are the ones a
+// plain `exact` launch produces).
+template <typename TT, typename ST>
+__global__ void __launch_bounds__(kThreads, 3)
+    measure_refine_kernel(const TT* __restrict__ tgt, const ST* __restrict__ src,
+                          const double* __restrict__ A, const double* __restrict__ B,
+                          const Geom g, Partial* __restrict__ part, const int* __restrict__ list,
+                          const int* __restrict__ count) {
+  const long long items = (long long)(*count) * g.ntiles;
+  for (long long w = blockIdx.x; w < items; w += gridDim.x) {
+    const long long p = list[w / g.ntiles];
+    const int tile = (int)(w % g.ntiles);
+    partials_cta<TT, ST, ER_LERP_EXACT>(tgt, src, A, B, g, p, tile, part + p * g.ntiles + tile);
+    __syncthreads();  // the reduction scratch is reused by the next item
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1004,16 +1042,36 @@ struct Affines {
 };
 
 // Per-particle finalize: kernels_numba.py:172-189 on the affine-corrected sums.
-__global__ void measure_finalize_kernel(const Partial* __restrict__ part, int ntiles,
-                                        long long P, const double* __restrict__ tmom,
-                                        double nvox, int overlap, Affines f,
-                                        double* __restrict__ ncc, uint8_t* __restrict__ degen,
-                                        int64_t* __restrict__ n_in) {
-  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (p >= P) return;
+//
+// Refinement (refine_list != NULL; the fp32-lerp paths): a particle whose
+// likelihood the fp32 samples cannot resolve to the north star's 1e-4 is
+// appended to refine_list, to be re-measured in reference-order fp64
+// (measure_refine_kernel) and finalized again (list mode, below).  The
+// fp32 samples carry errors of a few ulps of the STORED magnitudes (8-bit
+// data: bytes ~100 with the z-score's offset folded into gamma), so the
+// condition number uses the stored-magnitude scale as^2 XX in place of the
+// value-space sum of squares:
+//   kappa = as^2 XX / sss  +  at^2 YY / sst [fp32 target terms only]
+//           + 2 sqrt(as^2 XX * s_tt) / |sts|
+// (the condition number of z = sts^2 / (sst sss) under relative sample
+// perturbations, tools/fuzz_measure.py conditioning()).  Measured errors stay
+// below 0.7 eps kappa (100,000-case fuzz), so 4 eps32 kappa > 1e-4 (a 6x
+// margin) lists the particle, and so does any particle whose variance test
+// (< 1e-12, kernels_numba.py:183) is within 4 eps kappa of its threshold.
+struct RefineArgs {
+  int* list;         // NULL: no refinement
+  int* count;
+  int tgt_fp32;      // the target terms were accumulated in fp32
+};
+
+__device__ __forceinline__ void finalize_one(const Partial* __restrict__ q, int ntiles,
+                                             const double* __restrict__ tmom, double nvox,
+                                             int overlap, const Affines& f, long long p,
+                                             double* __restrict__ ncc,
+                                             uint8_t* __restrict__ degen,
+                                             int64_t* __restrict__ n_in, RefineArgs r) {
   double X = 0.0, XX = 0.0, YX = 0.0, Y = 0.0, YY = 0.0;
   long long n = 0;
-  const Partial* q = part + p * ntiles;
   for (int t = 0; t < ntiles; ++t) {
     X += q[t].x;
     XX += q[t].xx;
@@ -1045,13 +1103,55 @@ __global__ void measure_finalize_kernel(const Partial* __restrict__ part, int nt
   }
   const double sst = rn_sub(s_tt, rn_div(rn_mul(s_t, s_t), nf));
   const double sss = rn_sub(s_ss, rn_div(rn_mul(s_s, s_s), nf));
+  const double sts = rn_sub(s_ts, rn_div(rn_mul(s_t, s_s), nf));
+  if (r.list != nullptr && n > 0) {
+    const double e4 = 4.0 * 5.9604644775390625e-08;  // 4 eps32
+    const double xs = f.as * f.as * XX;                // stored-magnitude scale
+    const double yt = r.tgt_fp32 && overlap ? f.at * f.at * YY : 0.0;
+    const double ks = xs / fabs(sss);
+    const double kt = yt / fabs(sst);
+    const double kts = 2.0 * sqrt(xs * fmax(s_tt, 0.0)) / fabs(sts);
+    const double thr = 1e-12 * nf;
+    // the variance tests must not be decided by fp32 noise either
+    const bool near_s = fabs(sss - thr) <= e4 * xs;
+    const bool near_t = yt > 0.0 && fabs(sst - thr) <= e4 * yt;
+    const bool degenerate_sure = (sss < thr && !near_s) || (sst < thr && !near_t);
+    if (near_s || near_t || (!degenerate_sure && !(e4 * (ks + kt + kts) <= 1e-4))) {
+      r.list[atomicAdd(r.count, 1)] = (int)p;
+    }
+  }
   if (rn_div(sst, nf) < 1e-12 || rn_div(sss, nf) < 1e-12) {
     ncc[p] = 0.0;
     degen[p] = 1;
   } else {
-    const double sts = rn_sub(s_ts, rn_div(rn_mul(s_t, s_s), nf));
     ncc[p] = rn_div(rn_mul(sts, sts), rn_mul(sst, sss));
     degen[p] = 0;
+  }
+}
+
+__global__ void measure_finalize_kernel(const Partial* __restrict__ part, int ntiles,
+                                        long long P, const double* __restrict__ tmom,
+                                        double nvox, int overlap, Affines f,
+                                        double* __restrict__ ncc, uint8_t* __restrict__ degen,
+                                        int64_t* __restrict__ n_in, RefineArgs r) {
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  finalize_one(part + p * ntiles, ntiles, tmom, nvox, overlap, f, p, ncc, degen, n_in, r);
+}
+
+// finalize of the refined particles (list mode, persistent grid)
+__global__ void measure_finalize_list_kernel(const Partial* __restrict__ part, int ntiles,
+                                             const double* __restrict__ tmom, double nvox,
+                                             int overlap, Affines f, double* __restrict__ ncc,
+                                             uint8_t* __restrict__ degen,
+                                             int64_t* __restrict__ n_in,
+                                             const int* __restrict__ list,
+                                             const int* __restrict__ count) {
+  const int c = *count;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+    const long long p = list[i];
+    finalize_one(part + p * ntiles, ntiles, tmom, nvox, overlap, f, p, ncc, degen, n_in,
+                 RefineArgs{nullptr, nullptr, 0});
   }
 }
 
@@ -1125,10 +1225,18 @@ bool valid_volume(const er_volume* v) {
 
 }  // namespace
 
+// workspace: [P x ntiles partials][refine count (16 B)][refine list: P ints]
+static size_t partials_bytes(const Geom& g, int64_t P) {
+  return (size_t)P * (size_t)g.ntiles * sizeof(Partial);
+}
+static size_t workspace_need(const Geom& g, int64_t P) {
+  return partials_bytes(g, P) + 16 + (size_t)P * sizeof(int);
+}
+
 extern "C" size_t er_measure_workspace_bytes(const er_volume* tgt, int64_t P) {
   if (!tgt || tgt->nx < 1 || tgt->ny < 1 || P < 0) return 0;
   Geom g = make_geom(tgt, tgt);
-  return (size_t)P * (size_t)g.ntiles * sizeof(Partial);
+  return workspace_need(g, P);
 }
 
 extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
@@ -1146,7 +1254,7 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
   if (lerp_mode < ER_LERP_F32 || lerp_mode > ER_LERP_NEAREST)
     return er_set_error(ER_EINVAL, "er_measure_ncc: bad lerp_mode");
   const Geom g = make_geom(tgt, src);
-  const size_t need = (size_t)P * (size_t)g.ntiles * sizeof(Partial);
+  const size_t need = workspace_need(g, P);
   if (!workspace_dev || workspace_bytes < need)
     return er_set_error(ER_EINVAL, "er_measure_ncc: workspace too small");
   if ((long long)P * g.ntiles >= (1LL << 31))
@@ -1212,10 +1320,51 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
   Affines f{src->alpha, src->gamma, tgt->alpha, tgt->gamma};
   const double nvox = (double)tgt->nx * (double)tgt->ny * (double)tgt->nz;
   const int fb = 128;
+  // fp32-lerp samples (oct byte path, or the generic kernel on u8/f32 storage)
+  // are refined where they cannot resolve 1e-4 (measure_finalize_kernel);
+  // the bit-oct path samples exactly, nearest is a different operator, and
+  // f64-stored sources lerp in fp64 anyway
+  const bool refine = ER_REFINE && lerp_mode == ER_LERP_F32 && !use_bits && src->dtype != ER_F64;
+  RefineArgs r{nullptr, nullptr, tgt->dtype != ER_U8};
+  if (refine) {
+    char* base = (char*)workspace_dev + partials_bytes(g, P);
+    r.count = (int*)base;
+    r.list = (int*)(base + 16);
+    if (cudaMemsetAsync(r.count, 0, sizeof(int), st) != cudaSuccess) ER_CHECK_LAUNCH();
+  }
   measure_finalize_kernel<<<(unsigned)((P + fb - 1) / fb), fb, 0, st>>>(
       part, g.ntiles, P, tgt_moments_dev, nvox, overlap_only ? 1 : 0, f, ncc_dev, degen_dev,
-      n_in_dev);
+      n_in_dev, r);
   ER_CHECK_LAUNCH();
+  if (refine) {
+    long long grid = (long long)P * g.ntiles;
+    if (grid > 3LL * ER_NUM_SMS_B200) grid = 3LL * ER_NUM_SMS_B200;
+#define ER_REFINE_LAUNCH(TT, ST)                                                          \
+  measure_refine_kernel<TT, ST><<<(unsigned)grid, kThreads, 0, st>>>(                     \
+      (const TT*)tgt->data_dev, (const ST*)src->data_dev, A_dev, b_dev, g, part, r.list,  \
+      r.count)
+    if (src->dtype == ER_U8) {
+      switch (tgt->dtype) {
+        case ER_U8: ER_REFINE_LAUNCH(uint8_t, uint8_t); break;
+        case ER_F32: ER_REFINE_LAUNCH(float, uint8_t); break;
+        default: ER_REFINE_LAUNCH(double, uint8_t); break;
+      }
+    } else {
+      switch (tgt->dtype) {
+        case ER_U8: ER_REFINE_LAUNCH(uint8_t, float); break;
+        case ER_F32: ER_REFINE_LAUNCH(float, float); break;
+        default: ER_REFINE_LAUNCH(double, float); break;
+      }
+    }
+#undef ER_REFINE_LAUNCH
+    ER_CHECK_LAUNCH();
+    long long fgrid = (P + fb - 1) / fb;
+    if (fgrid > 16) fgrid = 16;
+    measure_finalize_list_kernel<<<(unsigned)fgrid, fb, 0, st>>>(
+        part, g.ntiles, tgt_moments_dev, nvox, overlap_only ? 1 : 0, f, ncc_dev, degen_dev,
+        n_in_dev, r.list, r.count);
+    ER_CHECK_LAUNCH();
+  }
   return ER_OK;
 }
 

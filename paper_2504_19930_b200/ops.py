@@ -62,7 +62,16 @@ def measure(tdv: DeviceVolume, sdv: DeviceVolume, A, B, overlap: bool, precision
     _lib.call("er_measure_ncc", tdv.desc_ptr, sdv.desc_ptr, ptr(tdv.moments), ptr(A), ptr(B),
               P, int(bool(overlap)), lerp_code(precision), ptr(ncc), ptr(degen), ptr(n_in),
               ptr(ws), ws.numel(), stream_ptr(dev))
+    if refines(sdv, precision):
+        _lib.launch_count += 2   # the refinement pass and its list finalize
     return ncc, degen, n_in
+
+
+def refines(sdv: DeviceVolume, precision: str) -> bool:
+    """Whether er_measure_ncc runs its fp64 refinement pass for this source
+    (fp32 lerps on a non-binary u8 or an f32-stored source)."""
+    return (precision == "f32" and sdv.dtype_code != _lib.ER_F64
+            and not sdv.desc.bitoct_dev)
 
 
 def _as_dv(v, device=None) -> DeviceVolume:
@@ -135,3 +144,13 @@ def smc_predict(states_in, states_out, seed, k, sigma, clip):
 
 def require(device=None):
     return require_cuda(device)
+
+
+def refined_count(tdv: DeviceVolume, P: int, workspace=None) -> int:
+    """Number of particles the last f32 measurement with this workspace
+    re-measured in fp64 (er_measure_ncc refinement; one sync).  Diagnostic."""
+    t = torch()
+    need = workspace_bytes(tdv, P)
+    ws = workspace if workspace is not None else WORKSPACE.get(require_cuda(), need)
+    off = need - 16 - 4 * int(P)
+    return int(ws[off:off + 4].view(t.int32).item())

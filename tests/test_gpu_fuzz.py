@@ -29,14 +29,15 @@ def test_random_warp_cases_match_the_oracle():
     assert not res["failures"], res["failures"][:5]
 
 
-def test_ill_conditioned_particles_are_within_their_conditioning():
-    """Two cases the 100k-case run found outside the f32 bar (seed 37): particles
-    with z ~ 1 on nearly constant overlaps, condition numbers 1.7e4 and 1e6.
-    Their errors must stay within 2 eps kappa (fuzz_measure.conditioning)."""
+def test_ill_conditioned_particles_meet_the_plain_f32_bar():
+    """Two cases the round-1 100k-case run found outside the f32 bar (seed 37):
+    particles with z ~ 1 on nearly constant overlaps, condition numbers 1.7e4
+    and 1e6.  The finalize now lists such particles and re-measures them in
+    fp64 (er_measure_ncc refinement), so they meet the plain 1e-4 bar with
+    bit-exact degenerate flags -- no conditioning allowance for f32."""
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     import fuzz_measure
 
-    res = fuzz_measure.run(n_cases=2693, seed=37, only={801, 2692})
+    res = fuzz_measure.run(n_cases=2693, seed=37, only={801, 2692}, strict=("f32",))
     assert not res["failures"], res["failures"]
-    cond = res["within_conditioning_only"]["f32"]
-    assert cond["particles"] >= 2 and cond["worst_rel_over_eps_kappa"] <= 2.0
+    assert res["within_conditioning_only"]["f32"]["particles"] == 0
