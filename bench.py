@@ -7,11 +7,11 @@ Workload (BASELINE.json configs[1], "C2"): image-based SMC on a synthetic
 the echo grid, quantised to 8 bit, z-scored), 2000 particles, ED frame.
 A *step* is one device-resident SMC iteration over the whole particle set:
 predict (Philox/ziggurat) -> index affines -> fused gather+NCC measurement ->
-[NCCL all-gather of z when N > 1] -> weights/ESS/systematic resampling/
-estimate.  ``value`` = particle-voxel evaluations (P x voxels, the
-reference's full-region count) per second over all ranks, inputs resident.
-L2 is flushed (256 MiB write) between timed steps; each step is timed with
-CUDA events on the launching stream, max over ranks.
+[one all-gather of the packed likelihoods when N > 1] -> weights/ESS/
+systematic resampling/estimate.  ``value`` = particle-voxel evaluations
+(P x voxels, the reference's full-region count) per second over all ranks,
+inputs resident.  L2 is flushed (256 MiB write) between timed steps; each
+step is timed with CUDA events on the launching stream, max over ranks.
 
 ``e2e``: the same metric through the public API -- one ``register_smc`` call
 per step (50 iterations, the reference default) on fresh volume objects, so
@@ -19,10 +19,15 @@ every step uploads both volumes from pinned host memory and reads the trace
 back (also reported as ``registration_ms_per_pair``, BASELINE's second
 metric); ``e2e.plugin_seam``: the reference's kernel-module seam on its host
 fp64 arrays.  ``roofline``: the measurement kernel against the measured HBM
-(and L2) bandwidth; ``precision_modes``: one launch per sampling mode.
-``--impl reference`` times the reference algorithm on the host CPU (the
-bit-exact C restatement in oracle/, all host threads) on a bounded particle
-sample of the same workload.
+copy bandwidth and against the L2 read bandwidth measured live in this run
+(er_probe_read); ``precision_modes``: one launch per sampling mode; ``c3``:
+register_sequence on a fresh 30-frame 4D pair (BASELINE configs[2]);
+``c5``: one 256^3 measurement at 16k particles (configs[4]).
+``--impl reference`` times the reference algorithm on the host CPU -- the
+bit-exact C restatement of kernels_numba._ncc_kernel in oracle/, all host
+threads, all 2000 particles per step -- on inputs built by oracle/ alone
+(oracle/phantom.py reproduces the reference generator's bytes; the product
+package is never imported on that path).
 """
 
 from __future__ import annotations
@@ -61,24 +66,15 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-modes", action="store_true", help="skip the per-precision-mode launches")
+    ap.add_argument("--no-configs", action="store_true", help="skip the c3 / c5 extra lines")
+    ap.add_argument("--c3-steps", type=int, default=1)
+    ap.add_argument("--c5-particles", type=int, default=16384)
     return ap.parse_args()
 
 
 def env_rank():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
-
-
-def l2_roofline(achieved_gbs):
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                        "l2_bandwidth.json")
-    try:
-        with open(path) as fh:
-            peak = float(json.load(fh)["l2_read_peak_gb_s"])
-    except (OSError, KeyError, ValueError):
-        return None
-    return {"peak": peak, "unit": "GB/s", "frac": achieved_gbs / peak,
-            "peak_source": "profiles/l2_bandwidth.json (tools/l2bw.cu, 52-96 MB resident)"}
 
 
 def cpu_model() -> str:
@@ -173,87 +169,81 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_rate(t, s, a, b, seconds, threads=0):
-    """Oracle (bit-exact C restatement of kernels_numba._ncc_kernel) on the
-    host cores over a bounded particle sample; returns (evals/s, sample, P, threads)."""
+def reference_inputs(P, seed=0):
+    """The C2 workload built by oracle/ alone (test infrastructure; never the
+    product package): the 8-bit echo pair from oracle/phantom.py (the
+    reference generator's bytes, tests/test_oracle_phantom.py), the
+    reference z-score (volume.py:119-130), and the index affines of SMC
+    iteration 0 (init + predict, seed 0, smc.py:145-174 via oracle/smc.py)."""
     from oracle import kernels as ok
+    from oracle import phantom as op
+    from oracle.smc import Cfg, affines_for, init_states, predict
 
     ok.build()
+    tq, sq, _, _ = op.echo_case(frames=1, seed=seed)
+    t = op.normalize_zscore(tq[0].astype(np.float64))
+    s = op.normalize_zscore(sq[0].astype(np.float64))
+    geom = (t.shape, op.ECHO_SPACING, (0.0, 0.0, 0.0))
+    cfg = Cfg(n_particles=P, seed=seed)
+    a, b = affines_for(predict(init_states(cfg), 0, cfg), geom, geom)
+    return {"t": t, "s": s, "a": a, "b": b, "dims": list(t.shape)}
+
+
+def cpu_reference_rate(inp, seconds, threads=0):
+    """The oracle (bit-exact C restatement of kernels_numba._ncc_kernel) on the
+    host cores over a bounded particle sample; returns (evals/s, particles,
+    seconds, threads)."""
+    from oracle import kernels as ok
+
     threads = threads or ok.max_threads()
-    nvox = t.data.size
-    p = max(threads, 8)
-    p = min(p, a.shape[0])
+    t, s, a, b = inp["t"], inp["s"], inp["a"], inp["b"]
+    nvox = t.size
+    p = min(max(threads, 8), a.shape[0])
     t0 = time.perf_counter()
-    ok.ncc_measure_batch(t.data, s.data, a[:p], b[:p], False, threads)
+    ok.ncc_measure_batch(t, s, a[:p], b[:p], False, threads)
     dt = time.perf_counter() - t0
     # scale the sample so one timed pass is ~`seconds` of CPU work
-    want = int(p * max(1.0, seconds / max(dt, 1e-3)))
-    want = max(p, min(want, a.shape[0]))
-    reps = max(1, math.ceil(want / a.shape[0]))
-    idx = np.arange(want) % a.shape[0]
+    want = max(p, min(int(p * max(1.0, seconds / max(dt, 1e-3))), a.shape[0]))
     t0 = time.perf_counter()
-    ok.ncc_measure_batch(t.data, s.data, a[idx], b[idx], False, threads)
+    ok.ncc_measure_batch(t, s, a[:want], b[:want], False, threads)
     dt = time.perf_counter() - t0
-    del reps
     return want * nvox / dt, want, dt, threads
 
 
-def first_iteration_affines(t, s, n, seed=0):
-    """Host copy of the particle set of SMC iteration 0 (init + predict, seed 0)."""
-    from paper_2504_19930_b200 import SmcConfig
-    from paper_2504_19930_b200.smc import init_particles, predict
-    from paper_2504_19930_b200.geometry import index_affine_batch, to_matrix, RigidParams
-
-    cfg = SmcConfig(n_particles=n, seed=seed)
-    ps = predict(init_particles(cfg), cfg)
-    center = t.physical_center()
-    mats = np.stack([to_matrix(RigidParams.from_array(r), center) for r in ps.states])
-    return index_affine_batch(mats, s.spacing, s.origin, t.spacing, t.origin)
-
-
 def run_reference(args):
+    """The reference arm: the reference's CPU implementation of the path (the
+    bit-exact C restatement in oracle/, on all host threads) measuring ALL
+    particles of the C2 workload per step; rank 0 only under torchrun."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    t, s, _ = make_workload()
     from oracle import kernels as ok
-    from oracle.smc import Cfg, affines_for, init_states, predict
 
-    cfg = Cfg(n_particles=args.particles, seed=0)
-    st = predict(init_states(cfg), 0, cfg)
-    a, b = affines_for(st, (t.dims, t.spacing, t.origin), (s.dims, s.spacing, s.origin))
-    ok.build()
+    inp = reference_inputs(args.particles)
     threads = ok.max_threads()
-    nvox = t.data.size
-    # bounded sample per step: one particle per thread x a small factor, so the
-    # whole --steps/--warmup run stays within a few minutes
-    p = min(a.shape[0], max(threads, 8) * 2)
-    t0 = time.perf_counter()
-    ok.ncc_measure_batch(t.data, s.data, a[:p], b[:p], False, threads)
-    one = time.perf_counter() - t0
-    budget = 150.0 / max(1, args.steps + args.warmup)
-    p = min(a.shape[0], max(threads, int(p * budget / max(one, 1e-3))))
+    t, s, a, b = inp["t"], inp["s"], inp["a"], inp["b"]
+    nvox = t.size
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        ok.ncc_measure_batch(t.data, s.data, a[:p], b[:p], False, threads)
+        ok.ncc_measure_batch(t, s, a, b, False, threads)
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
     ms = 1e3 * sum(times) / len(times)
-    value = p * nvox / (ms * 1e-3)
-    sample = (f"ncc_measure_batch of the first {p} particles of SMC iteration 0 on the C2 "
-              f"176x176x208 pair (full region), {threads} threads, C oracle "
-              f"(bit-exact restatement of kernels_numba._ncc_kernel)")
+    value = args.particles * nvox / (ms * 1e-3)
+    sample = (f"ncc_measure_batch of all {args.particles} particles of SMC iteration 0 on the "
+              f"C2 176x176x208 pair (full region) per step, {threads} threads, C oracle "
+              f"(bit-exact restatement of kernels_numba._ncc_kernel); inputs from oracle/ "
+              f"(the reference generator's bytes)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "particles_sampled": p, "voxels": nvox,
-                   "host_threads": threads},
+        "config": {"workload": WORKLOAD, "particles": args.particles, "voxels": nvox,
+                   "volume_dims": inp["dims"], "host_threads": threads},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "cpu_model": cpu_model(),
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -278,6 +268,48 @@ def measured_peaks():
         except Exception:
             pass
     return 6650.0, "fallback"
+
+
+def l2_peak_live(dev, mb=64, reads_gb=8.0):
+    """L2 read bandwidth measured in this run on this GPU (er_probe_read: every
+    SM streams an L2-resident buffer with 8-byte lane loads -- the oct gather
+    width -- through L2); best of 3 launches that each read ``reads_gb`` GB."""
+    import torch
+
+    from paper_2504_19930_b200 import _lib
+    from paper_2504_19930_b200.device import ptr
+
+    nbytes = mb << 20
+    buf = torch.ones(nbytes // 8, dtype=torch.float64, device=dev)
+    sink = torch.zeros(1, dtype=torch.int32, device=dev)
+    reps = max(1, int(reads_gb * 1e9 / nbytes))
+    stream = torch.cuda.current_stream(dev)
+    best = 0.0
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _lib.call("er_probe_read", ptr(buf), nbytes, reps, ptr(sink), stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        best = max(best, nbytes * reps / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del buf
+    return {"peak": best, "unit": "GB/s", "buffer_mb": mb,
+            "peak_source": f"measured live in this run: er_probe_read, {mb} MiB L2-resident "
+                           f"buffer, 8-byte lane loads, {reps} passes per launch, best of 4"}
+
+
+def first_iteration_affines(t, s, n, seed=0):
+    """Host copy of the index affines of SMC iteration 0 (init + predict,
+    seed 0) through the package's host geometry (the plugin-seam leg)."""
+    from paper_2504_19930_b200 import SmcConfig
+    from paper_2504_19930_b200.geometry import RigidParams, index_affine_batch, to_matrix
+    from paper_2504_19930_b200.smc import init_particles, predict
+
+    cfg = SmcConfig(n_particles=n, seed=seed)
+    ps = predict(init_particles(cfg), cfg)
+    center = t.physical_center()
+    mats = np.stack([to_matrix(RigidParams.from_array(r), center) for r in ps.states])
+    return index_affine_batch(mats, s.spacing, s.origin, t.spacing, t.origin)
 
 
 def run_ours(args):
@@ -312,7 +344,7 @@ def run_ours(args):
           for _ in range(n_steps)]
     mev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(n_steps)]
-    n_in_sum = []
+    n_in = []
 
     def one_step(k):
         # identical code for warm-up and timed steps (first-use costs such as
@@ -323,9 +355,11 @@ def run_ours(args):
         mev[k][0].record(stream)
         run.measure()
         mev[k][1].record(stream)
-        n_in_sum.append(run.n_local[: run.plan.count].sum())
         run.update(k)
         ev[k][1].record(stream)
+        # sampled-voxel count of this step, reduced AFTER its end event (a
+        # reduction launched inside the window would be timed with the step)
+        n_in.append(run.n_local[: run.plan.count].sum())
 
     for k in range(args.warmup):
         one_step(k)
@@ -340,7 +374,7 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
     launches = _lib.launch_count - launches0
     ev, mev = ev[args.warmup:], mev[args.warmup:]
-    n_in_sum = n_in_sum[args.warmup:]
+    n_in = n_in[args.warmup:]
     step_ms = [a.elapsed_time(b) for a, b in ev]
     meas_ms = [a.elapsed_time(b) for a, b in mev]
     pre_ms = [a[0].elapsed_time(b[0]) for a, b in zip(ev, mev)]
@@ -350,21 +384,27 @@ def run_ours(args):
         torch.distributed.all_reduce(total, op=torch.distributed.ReduceOp.MAX)
     total_ms = float(total.item())
     ms_per_step = total_ms / args.steps
-    value = P * nvox * args.steps / (total_ms * 1e-3)
-    sampled = float(sum(float(x.item()) for x in n_in_sum)) / max(1, len(n_in_sum))
+    value = P * nvox / (ms_per_step * 1e-3)
+    sampled = float(sum(float(x.item()) for x in n_in)) / max(1, len(n_in))
     meas_avg = sum(meas_ms) / max(1, len(meas_ms))
     bytes_per_unit = 8 * run.sdv.storage.element_size() + run.tdv.storage.element_size()
     peak, peak_kind = measured_peaks()
     achieved_gbs = sampled * bytes_per_unit / (meas_avg * 1e-3) / 1e9
     traffic = load_traffic()
+    l2 = l2_peak_live(dev) if world == 1 else None
+    if l2 is not None:
+        l2["frac"] = achieved_gbs / l2["peak"]
     roofline = {
         "bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
         "frac": achieved_gbs / peak,
         "traffic": (traffic or {}).get("dram_bytes_per_launch"),
         "kernel": "measure_oct_kernel<u8, lerp f32> (+ measure_finalize_kernel)",
-        # secondary denominator: the sources are L2-resident;
-        # L2 read bandwidth measured by tools/l2bw.cu (profiles/l2_bandwidth.json)
-        "l2": l2_roofline(achieved_gbs),
+        "note": ("achieved = sampled (in-bounds) voxels x 9 algorithmic bytes (8 oct "
+                 "corner bytes + 1 target byte) / measurement time: an HBM-equivalent "
+                 "rate.  Both volumes are L2-resident, so the DRAM traffic per launch "
+                 "(`traffic`, ncu) is only the compulsory volume reads; `l2` is the same "
+                 "rate against the L2 read bandwidth measured live in this run."),
+        "l2": l2,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
         "bytes_per_sampled_voxel": bytes_per_unit,
         "sampled_voxels_per_launch": sampled,
@@ -373,8 +413,8 @@ def run_ours(args):
         "kernel_share_of_step": meas_avg / ms_per_step,
         "pre_ms_per_step": sum(pre_ms) / len(pre_ms),
         "post_ms_per_step": sum(post_ms) / len(post_ms),
-        "post_ms_steps": [round(x, 3) for x in post_ms],
     }
+    refined = int(ops_refined(run))
     clk = clocks.summary()
     modes = precision_modes(run, P, nvox, dev) if world == 1 and not args.no_modes else None
 
@@ -384,16 +424,20 @@ def run_ours(args):
         e2e = run_e2e(args, t, s, ex, dev, world)
         if world == 1:
             e2e["plugin_seam"] = run_plugin_seam(args, t, s, dev)
+    extra = {}
+    if world == 1 and not args.no_configs:
+        extra["c3"] = run_c3(args, dev)
+        extra["c5"] = run_c5(args, dev, peak, l2)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        a, b = first_iteration_affines(t, s, P)
-        rate, sample_p, secs, threads = cpu_reference_rate(t, s, a, b, args.cpu_seconds)
+        inp = reference_inputs(P)
+        rate, sample_p, secs, threads = cpu_reference_rate(inp, args.cpu_seconds)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                "cpu_model": cpu_model(),
-               "sample": (f"{sample_p} particles of SMC iteration 0 (C2 pair, full region) "
-                          f"through the C oracle (bit-exact restatement of "
-                          f"kernels_numba._ncc_kernel), {secs:.1f} s on {threads} host "
+               "sample": (f"{sample_p} particles of SMC iteration 0 (C2 pair, full region; "
+                          f"inputs from oracle/) through the C oracle (bit-exact restatement "
+                          f"of kernels_numba._ncc_kernel), {secs:.1f} s on {threads} host "
                           f"threads")}
     if rank == 0:
         line = {
@@ -407,12 +451,20 @@ def run_ours(args):
                        "step": "one device SMC iteration (predict+affine+measure+update)",
                        "parallelism": f"particles sharded over {world} GPU(s)"},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "refined_particles_last_step": refined,
             "precision_modes": modes,
             "gpu_launches": launches,
+            **extra,
         }
         emit(line)
     if launched:
         torch.distributed.destroy_process_group()
+
+
+def ops_refined(run):
+    from paper_2504_19930_b200 import ops
+
+    return ops.refined_count(run.tdv, run.plan.count, run.ws)
 
 
 def precision_modes(run, P, nvox, dev):
@@ -446,13 +498,14 @@ def run_plugin_seam(args, t, s, dev):
     reference passes (kernels_numba.py:203) -- the z-scored 8-bit volumes,
     recognised on the device as an affine image of bytes (oct fast path).
     ``value``: per call with the same array objects, as the reference's SMC
-    loop passes them every iteration (device copies cached and re-validated
-    by fingerprint; affines uploaded, results read back every call).
-    ``cold``: the first call on fresh arrays (both fp64 volumes uploaded and
-    classified inside the timed region)."""
+    loop passes them every iteration (device copies cached, re-validated by
+    a full-content digest every call; affines uploaded, results read back every
+    call).  ``cold``: the first call on fresh arrays (both fp64 volumes uploaded
+    and classified inside the timed region)."""
     import torch
 
-    from paper_2504_19930_b200 import kernels_sm100
+    from paper_2504_19930_b200 import kernels_sm100, ops
+    from paper_2504_19930_b200.device import device_volume
 
     a, b = first_iteration_affines(t, s, args.particles)
     tgt = np.ascontiguousarray(t.data)
@@ -476,16 +529,36 @@ def run_plugin_seam(args, t, s, dev):
     sec = sum(times) / len(times)
     csec = min(cold)
     evals = args.particles * tgt.size
-    return {"value": evals / sec, "unit": UNIT,
+    # the same particles' in-bounds voxel count (one untimed device measurement)
+    A = torch.as_tensor(np.ascontiguousarray(a).reshape(-1, 9), device=dev)
+    B = torch.as_tensor(np.ascontiguousarray(b).reshape(-1, 3), device=dev)
+    sampled = float(ops.measure(device_volume(t, dev), device_volume(s, dev), A, B, False,
+                                "f32")[2].sum().item())
+    return {"value": evals / sec, "unit": UNIT, "sampled_voxels_per_s": sampled / sec,
             "h2d_bytes_per_step": int(a.nbytes + b.nbytes),
             "d2h_bytes_per_step": int(z.nbytes + d.nbytes),
             "step": "kernels_sm100.ncc_measure_batch on the reference's host fp64 arrays "
                     "(kernel-module seam), 2000 particles, same array objects every call "
-                    "(volumes cached on the device, fingerprint-checked)",
-            "cold": {"value": evals / csec, "unit": UNIT,
+                    "(volumes cached on the device, content digest re-checked every call)",
+            "cold": {"value": evals / csec, "unit": UNIT, "sampled_voxels_per_s": sampled / csec,
                      "h2d_bytes_per_step": int(tgt.nbytes + src.nbytes + a.nbytes + b.nbytes),
                      "step": "first call on fresh arrays: fp64 upload + on-device byte-"
                              "lattice recognition + oct build + measurement"}}
+
+
+def _pinned_copy(v):
+    """A fresh Volume3 with the same content and no device cache; 8-bit codec
+    volumes get their raw bytes in pinned host memory."""
+    import torch
+
+    c = copy.copy(v)
+    if hasattr(c, "_er_device_cache"):
+        object.__delattr__(c, "_er_device_cache")
+    if v.codec is not None:
+        raw = torch.empty(v.codec.raw.shape, dtype=torch.uint8, pin_memory=True)
+        raw.numpy()[...] = v.codec.raw
+        object.__setattr__(c, "codec", type(v.codec)(raw.numpy(), v.codec.mean, v.codec.std))
+    return c
 
 
 def run_e2e(args, t, s, ex, dev, world):
@@ -493,28 +566,17 @@ def run_e2e(args, t, s, ex, dev, world):
     import torch
 
     from paper_2504_19930_b200 import SmcConfig, register_smc
+    from paper_2504_19930_b200 import smc as dsmc
 
     P = args.particles
     cfg = SmcConfig(mode="image", n_particles=P, n_iterations=args.e2e_iters, seed=0)
-
-    def pinned_copy(v):
-        c = copy.copy(v)
-        if hasattr(c, "_er_device_cache"):
-            object.__delattr__(c, "_er_device_cache")
-        if v.codec is not None:
-            raw = torch.empty(v.codec.raw.shape, dtype=torch.uint8, pin_memory=True)
-            raw.numpy()[...] = v.codec.raw
-            object.__setattr__(c, "codec", type(v.codec)(raw.numpy(), v.codec.mean,
-                                                         v.codec.std))
-        return c
-
     h2d = (t.codec.raw.nbytes + s.codec.raw.nbytes) if t.codec is not None else \
         (t.data.nbytes + s.data.nbytes)
     d2h = args.e2e_iters * 12 * 8 + 64
     times = []
     est = None
     for i in range(1 + args.e2e_steps):  # first call is warm-up
-        tc, sc = pinned_copy(t), pinned_copy(s)
+        tc, sc = _pinned_copy(t), _pinned_copy(s)
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
@@ -529,12 +591,105 @@ def run_e2e(args, t, s, ex, dev, world):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
     sec = float(tt.item()) / len(times)
     evals = P * t.data.size * args.e2e_iters
-    return {"value": evals / sec, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+    # sampled voxels of the same registration (deterministic): an untimed
+    # replay of its iterations summing the in-bounds counts
+    run = dsmc.DeviceSmcRun(t, s, cfg, ex)
+    counts = []
+    for k in range(cfg.n_iterations):
+        run.step(k)
+        counts.append(run.n_local[: run.plan.count].sum())
+    sampled = float(sum(float(c.item()) for c in counts))
+    if world > 1:
+        st = torch.tensor([sampled], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(st)
+        sampled = float(st.item())
+    return {"value": evals / sec, "unit": UNIT, "sampled_voxels_per_s": sampled / sec,
+            "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": len(times),
             "step": f"register_smc on fresh volumes, {args.e2e_iters} iterations",
             "registration_ms_per_pair": sec * 1e3,
             "estimate_deg_mm": [math.degrees(x) for x in est.to_array()[:3]]
             + list(est.to_array()[3:])}
+
+
+def run_c3(args, dev):
+    """BASELINE configs[2] through the public API: register_sequence (mask-mode
+    SMC 2000 x 50 on the ED masks, then warp + score all 30 frames) on a fresh
+    30-frame 176x176x208 pair whose frames and masks start in host memory
+    (uploads inside the timed region).  One warm-up call, then timed calls."""
+    import torch
+
+    from paper_2504_19930_b200 import Executor, Sequence4, SmcConfig, Volume3, register_sequence
+    from paper_2504_19930_b200.phantom_device import echo_case_device
+
+    case = echo_case_device(frames=30, seed=0)
+
+    def fresh(vols):
+        return [Volume3.from_u8(v.codec.raw.copy(), v.spacing, v.origin) for v in vols]
+
+    cfg = SmcConfig(mode="mask", n_particles=2000, n_iterations=50, seed=0)
+    h2d = sum(v.codec.raw.nbytes for v in (*case.target.frames, *case.source.frames,
+                                           *case.target_masks, *case.source_masks))
+    walls = []
+    rep = None
+    for i in range(1 + max(1, args.c3_steps)):
+        ft = Sequence4(fresh(case.target.frames), frame_rate=case.target.frame_rate)
+        fs = Sequence4(fresh(case.source.frames), frame_rate=case.source.frame_rate)
+        ftm, fsm = fresh(case.target_masks), fresh(case.source_masks)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        rep = register_sequence(ft, fs, ftm, fsm, cfg, Executor(device=dev.index))
+        torch.cuda.synchronize(dev)
+        if i > 0:
+            walls.append(time.perf_counter() - t0)
+    sec = sum(walls) / len(walls)
+    return {"workload": "C3: mask-mode SMC (2000 x 50) on the ED masks + warp/score of a "
+                        "30-frame 176x176x208 4D cycle (register_sequence)",
+            "ms_per_4d_pair": sec * 1e3, "steps": len(walls),
+            "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(50 * 12 * 8 + 30 * 6 * 8),
+            "dsc_before_mean": rep.aggregates["dsc_before_mean"],
+            "dsc_after_mean": rep.aggregates["dsc_after_mean"],
+            "estimate_deg_mm": rep.estimate_deg_mm}
+
+
+def run_c5(args, dev, hbm_peak, l2):
+    """BASELINE configs[4] at 16k particles on 256^3: one measurement launch of
+    SMC iteration 0's particles (after a warm-up launch), CUDA events."""
+    import torch
+
+    from paper_2504_19930_b200 import Executor, SmcConfig, normalize_zscore
+    from paper_2504_19930_b200 import smc as dsmc
+    from paper_2504_19930_b200.phantom_device import echo_case_device
+
+    P = args.c5_particles
+    case = echo_case_device(dims=(256, 256, 256), spacing=(0.8, 0.8, 0.8), frames=1, seed=0)
+    t = normalize_zscore(case.target.frames[0])
+    s = normalize_zscore(case.source.frames[0])
+    run = dsmc.DeviceSmcRun(t, s, SmcConfig(mode="image", n_particles=P, n_iterations=1,
+                                            seed=0), Executor(device=dev.index))
+    run.predict(0)
+    run.measure()
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    ms = []
+    for _ in range(2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run.measure()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms.append(e0.elapsed_time(e1))
+    m = min(ms)
+    nin = float(run.n_local[:P].sum().item())
+    gbs = nin * 9 / (m * 1e-3) / 1e9
+    return {"workload": "C5: 256^3 z-scored u8 echo pair, SMC iteration-0 particles, one "
+                        "measurement launch",
+            "particles": P, "kernel_ms": m, "evals_per_s": P * t.data.size / (m * 1e-3),
+            "sampled_voxels_per_s": nin / (m * 1e-3),
+            "roofline": {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": gbs / hbm_peak,
+                         "l2_frac": gbs / l2["peak"] if l2 else None}}
 
 
 _RESULT_OUT = None

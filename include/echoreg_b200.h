@@ -62,6 +62,14 @@ const char *er_last_error(void);
  * does not allow. */
 int er_debug_bounds_faults(unsigned long long *count);
 
+/* Measurement infrastructure (no reference counterpart): one launch reading
+ * the first `bytes` of buf_dev `reps` times with 8-byte lane loads through L2
+ * (every SM, 4 loads in flight per thread).  Timed by the caller with events
+ * on `stream`; bench.py uses it for the live L2 roofline denominator.
+ * sink_dev: 4 bytes of device scratch. */
+int er_probe_read(const void *buf_dev, int64_t bytes, int32_t reps, void *sink_dev,
+                  void *stream);
+
 /* ---- volumes ---------------------------------------------------------- */
 
 /* Stored-value moments: out_dev[0] = sum(stored), out_dev[1] = sum(stored^2),
@@ -208,6 +216,18 @@ int er_smc_update(const double *z_dev, const uint8_t *degen_dev, double *weights
                   double *scratch_dev /* n doubles: cumulative weights */, int64_t n, double beta, double ess_fraction, uint64_t seed, int64_t k,
                   int32_t estimate_best, er_smc_ctl *ctl_dev, double *trace_row_dev,
                   void *stream);
+
+/* er_smc_update reading the result of the ONE all-gather per iteration of a
+ * particle-sharded run: zd_dev holds world blocks of
+ * block_bytes, rank r's block = [z: shard f64 | degenerate flags: shard u8 |
+ * pad to 8 B]; particle i = r * shard + j.  Identical outputs to
+ * er_smc_update on the unpacked arrays.  block_bytes >= 9 * shard, % 8 == 0. */
+int er_smc_update_gathered(const void *zd_dev, int64_t shard, int64_t block_bytes,
+                           double *weights_dev, const double *states_in_dev,
+                           double *states_out_dev, double *z_out_dev, double *scratch_dev,
+                           int64_t n, double beta, double ess_fraction, uint64_t seed, int64_t k,
+                           int32_t estimate_best, er_smc_ctl *ctl_dev, double *trace_row_dev,
+                           void *stream);
 
 /* ---- warp / scoring of frames (geometry.py:188-200, metrics.py) -------- */
 

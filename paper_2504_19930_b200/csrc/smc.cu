@@ -262,8 +262,32 @@ __device__ double block_exclusive_scan(double v, double* sh) {
   return sh[warp] + (incl - v);
 }
 
+// Where the update reads particle i's likelihood and degenerate flag:
+// contiguous arrays (one GPU, or the caller gathered them), or the rank blocks
+// of ONE all-gather of packed per-rank buffers [z: shard f64 | flags: shard
+// u8 | pad], block bytes apart (the single collective per iteration).
+struct ZContig {
+  const double* __restrict__ z;
+  const uint8_t* __restrict__ degen;
+  __device__ __forceinline__ double zv(long long i) const { return z[i]; }
+  __device__ __forceinline__ double dg(long long i) const { return degen ? (double)degen[i] : 0.0; }
+};
+struct ZPacked {
+  const unsigned char* __restrict__ base;
+  long long shard, block;
+  __device__ __forceinline__ double zv(long long i) const {
+    const long long r = i / shard;
+    return reinterpret_cast<const double*>(base + r * block)[i - r * shard];
+  }
+  __device__ __forceinline__ double dg(long long i) const {
+    const long long r = i / shard;
+    return (double)base[r * block + 8 * shard + (i - r * shard)];
+  }
+};
+
+template <typename ZA>
 __global__ void __launch_bounds__(kUpdThreads)
-    smc_update_kernel(const double* __restrict__ z, const uint8_t* __restrict__ degen,
+    smc_update_kernel(const ZA za,
                       double* __restrict__ w, const double* __restrict__ st_in,
                       double* __restrict__ st_out, double* __restrict__ z_out,
                       double* __restrict__ cw, long long n, double beta, double ess_frac,
@@ -287,8 +311,8 @@ __global__ void __launch_bounds__(kUpdThreads)
   long long bi = 1LL << 62;
   double ndeg = 0.0;
   for (long long i = lo; i < hi; ++i) {
-    better(bv, bi, z[i], i);
-    ndeg += degen ? (double)degen[i] : 0.0;
+    better(bv, bi, za.zv(i), i);
+    ndeg += za.dg(i);
   }
   block_argmax(bv, bi, shv, shi);
   if (tid == 0 && bv > ctl->best_measurement) {
@@ -301,7 +325,7 @@ __global__ void __launch_bounds__(kUpdThreads)
   const double m = rn_mul(beta, bv);
   double part = 0.0;
   for (long long i = lo; i < hi; ++i) {
-    const double wi = rn_mul(w[i], exp(rn_sub(rn_mul(beta, z[i]), m)));
+    const double wi = rn_mul(w[i], exp(rn_sub(rn_mul(beta, za.zv(i)), m)));
     w[i] = wi;
     part += wi;
   }
@@ -354,7 +378,7 @@ __global__ void __launch_bounds__(kUpdThreads)
       const long long idx = a < n - 1 ? a : n - 1;
 #pragma unroll
       for (int d = 0; d < 6; ++d) st_out[6 * i + d] = st_in[6 * idx + d];
-      z_out[i] = z[idx];
+      z_out[i] = za.zv(idx);
     }
     __syncthreads();
     for (long long i = lo; i < hi; ++i) w[i] = inv_n;
@@ -362,7 +386,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     for (long long i = lo; i < hi; ++i) {
 #pragma unroll
       for (int d = 0; d < 6; ++d) st_out[6 * i + d] = st_in[6 * i + d];
-      z_out[i] = z[i];
+      z_out[i] = za.zv(i);
     }
   }
   __syncthreads();
@@ -543,9 +567,29 @@ extern "C" int er_smc_update(const double* z_dev, const uint8_t* degen_dev, doub
       !scratch_dev || !ctl_dev || !trace_row_dev || n < 1)
     return er_set_error(ER_EINVAL, "er_smc_update: args");
   if (beta < 0) return er_set_error(ER_EINVAL, "er_smc_update: beta must be >= 0");
-  smc_update_kernel<<<1, kUpdThreads, 0, as_stream(stream)>>>(
-      z_dev, degen_dev, weights_dev, states_in_dev, states_out_dev, z_out_dev, scratch_dev, n,
-      beta, ess_fraction, seed, k, estimate_best, ctl_dev, trace_row_dev);
+  smc_update_kernel<ZContig><<<1, kUpdThreads, 0, as_stream(stream)>>>(
+      ZContig{z_dev, degen_dev}, weights_dev, states_in_dev, states_out_dev, z_out_dev,
+      scratch_dev, n, beta, ess_fraction, seed, k, estimate_best, ctl_dev, trace_row_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" int er_smc_update_gathered(const void* zd_dev, int64_t shard, int64_t block_bytes,
+                                      double* weights_dev, const double* states_in_dev,
+                                      double* states_out_dev, double* z_out_dev,
+                                      double* scratch_dev, int64_t n, double beta,
+                                      double ess_fraction, uint64_t seed, int64_t k,
+                                      int32_t estimate_best, er_smc_ctl* ctl_dev,
+                                      double* trace_row_dev, void* stream) {
+  if (!zd_dev || !weights_dev || !states_in_dev || !states_out_dev || !z_out_dev ||
+      !scratch_dev || !ctl_dev || !trace_row_dev || n < 1 || shard < 1 ||
+      block_bytes < 9 * shard || block_bytes % 8 != 0)
+    return er_set_error(ER_EINVAL, "er_smc_update_gathered: args");
+  if (beta < 0) return er_set_error(ER_EINVAL, "er_smc_update_gathered: beta must be >= 0");
+  smc_update_kernel<ZPacked><<<1, kUpdThreads, 0, as_stream(stream)>>>(
+      ZPacked{(const unsigned char*)zd_dev, shard, block_bytes}, weights_dev, states_in_dev,
+      states_out_dev, z_out_dev, scratch_dev, n, beta, ess_fraction, seed, k, estimate_best,
+      ctl_dev, trace_row_dev);
   ER_CHECK_LAUNCH();
   return ER_OK;
 }

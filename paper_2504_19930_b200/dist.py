@@ -69,6 +69,35 @@ def allgather_shards(local, plan: ShardPlan, out):
     return out[: plan.n]
 
 
+def packed_block_bytes(shard: int) -> int:
+    """Bytes of one rank's packed block [z: shard f64 | flags: shard u8 | pad
+    to 8] (er_smc_update_gathered)."""
+    return -(-(9 * shard) // 8) * 8
+
+
+def allgather_packed(local, out):
+    """The one collective of an SMC iteration: every rank's packed uint8
+    block into ``out`` (world blocks, rank order).  Under a host-staged
+    process group (gloo, the CPU tests and the single-GPU multi-rank test)
+    the device block is staged through host memory."""
+    return allgather_tensor(local, out)
+
+
+def allgather_tensor(local, out):
+    """all_gather_into_tensor on the default group: NCCL directly on device
+    tensors; other backends (gloo) through host memory."""
+    import torch.distributed as td
+
+    if td.get_backend() == "nccl" or local.device.type == "cpu":
+        td.all_gather_into_tensor(out, local)
+        return out
+    host = local.cpu()
+    gathered = host.new_empty(out.numel())
+    td.all_gather_into_tensor(gathered, host)
+    out.copy_(gathered)
+    return out
+
+
 def allgather_rows(local, plan: ShardPlan):
     """Gather every rank's padded (plan.shard, k) float64 block of host rows
     (numpy) and return the first plan.n rows, in rank order.  Used for the

@@ -110,10 +110,8 @@ def register_exhaustive(target: Volume3, source: Volume3, g: GridSpec,
                               executor.precision, out=tuple(o[:cnt] for o in out))
         _lib.call("er_argmax_update", ptr(z), cnt, start, ptr(best), st)
     if w > 1:
-        import torch.distributed as td
-
         allb = t.empty(2 * w, **f64)
-        td.all_gather_into_tensor(allb, best)
+        dist.allgather_tensor(best, allb)
         pairs = allb.view(w, 2).cpu().numpy()
         best_value, best_index = -1.0, -1
         for v, i in pairs:  # ranks hold increasing node ranges: strict '>' keeps lowest

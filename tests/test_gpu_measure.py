@@ -253,6 +253,40 @@ def test_kernel_module_seam_revalidates_mutated_volumes():
     assert [dv.dtype_code for dv in dvs] == [_lib.ER_F64]   # re-uploaded, exact storage
 
 
+def test_kernel_module_seam_sees_any_in_place_edit():
+    """The device copies are validated against the FULL content of the host
+    arrays (Volume3.data is writable, /root/reference/pkg/src/echoreg/volume.py:
+    32-47): an edit of one interior voxel of either volume -- on the byte
+    lattice, so the storage type does not change -- and of the warp's source
+    must show up in the next call's results."""
+    from paper_2504_19930_b200 import kernels_sm100
+
+    t = _zscored_bytes((30, 20, 26), 17)
+    s = _zscored_bytes((30, 20, 26), 18)
+    a, b = _near_identity_affines(12, 19, shift=0.5)
+    z_prev, _ = kernels_sm100.ncc_measure_batch(t, s, a, b, False)
+    # one byte step of each volume's lattice (taken before any edit)
+    steps = {id(v): float(np.min(np.diff(np.unique(v)))) for v in (t, s)}
+    for vol, idx in ((s, (17, 11, 13)), (t, (13, 7, 19)), (s, (12, 9, 8))):
+        step = steps[id(vol)]
+        vol[idx] += step if vol[idx] < vol.max() else -step
+        z, d = kernels_sm100.ncc_measure_batch(t, s, a, b, False)
+        # bitwise what a fresh upload of the edited arrays gives, and not the
+        # stale result
+        z_fresh, d_fresh = kernels_sm100.ncc_measure_batch(t.copy(), s.copy(), a, b, False)
+        assert np.array_equal(z, z_fresh) and np.array_equal(d, d_fresh), idx
+        assert not np.array_equal(z, z_prev), idx
+        zo, do = ok.ncc_measure_batch(t, s, a, b, False)
+        assert _close(z, zo, RTOL["f32"])[0], idx
+        assert np.array_equal(d, do)
+        z_prev = z
+    w = np.arange(30 * 20 * 26, dtype=np.float64).reshape(30, 20, 26)
+    eye, zero = np.eye(3), np.zeros(3)
+    kernels_sm100.resample_trilinear(w, eye, zero, w.shape)
+    w[21, 9, 4] = -5.0
+    assert np.array_equal(kernels_sm100.resample_trilinear(w, eye, zero, w.shape), w)
+
+
 def test_lattice_recognition_rejects_other_data():
     from paper_2504_19930_b200 import _lib
     from paper_2504_19930_b200.device import device_volume_from_array
