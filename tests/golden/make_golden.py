@@ -339,10 +339,117 @@ def pipeline_cases():
     print("pipeline.npz")
 
 
+def zscore_cases():
+    """normalize_zscore on 8-bit data (volume.py:119-130): the reference's mean,
+    population std and normalised values for byte volumes of several shapes
+    and level distributions."""
+    rng = np.random.default_rng(2024)
+    out = {}
+    shapes = [(5, 6, 7), (17, 9, 23), (40, 36, 44), (64, 64, 64), (88, 88, 104)]
+    for i, dims in enumerate(shapes):
+        for j, kind in enumerate(("uniform", "skewed", "sparse")):
+            if kind == "uniform":
+                raw = rng.integers(0, 256, dims)
+            elif kind == "skewed":
+                raw = np.clip(np.round(rng.lognormal(3.0, 0.8, dims)), 0, 255)
+            else:
+                raw = np.where(rng.random(dims) < 0.1, rng.integers(1, 256, dims), 0)
+            raw = raw.astype(np.uint8)
+            v = Volume3(raw.astype(np.float64))
+            z = normalize_zscore(v)
+            key = f"v{i}_{kind}"
+            out[f"{key}__raw"] = raw
+            out[f"{key}__mean"] = np.array(float(v.data.mean()))
+            out[f"{key}__std"] = np.array(float(v.data.std()))
+            if raw.size <= 64 ** 3:
+                out[f"{key}__z"] = z.data
+    np.savez_compressed(os.path.join(OUT, "zscore.npz"), **out)
+    print("zscore.npz", len(out))
+
+
+def report_cases():
+    """RegistrationReport JSON (pipeline.py:32-76), percentile_summary and its
+    CSV (pipeline.py:273-308), written by the reference itself."""
+    import json
+
+    from echoreg.pipeline import (RegistrationReport, percentile_summary,
+                                  write_summary_csv)
+
+    rng = np.random.default_rng(77)
+    reports = []
+    for c in range(9):
+        nf = int(rng.integers(2, 6))
+        before = [float(x) for x in rng.uniform(0.5, 0.9, nf)]
+        after = [float(min(1.0, b + d)) for b, d in zip(before, rng.uniform(-0.05, 0.3, nf))]
+        if c == 3:
+            before[1] = after[1] = None          # a frame without masks
+        if c == 5:
+            before = [None] * nf                 # no DSC at all: excluded from the summary
+            after = [None] * nf
+        ncc_b = [float(x) for x in rng.uniform(0.1, 0.6, nf)]
+        ncc_a = [float(x) for x in rng.uniform(0.4, 0.95, nf)]
+        from echoreg.pipeline import _aggregates
+
+        rep = RegistrationReport(
+            mode="mask", method="smc", config={"n_particles": 64, "seed": c},
+            estimate_deg_mm={"rx_deg": 1.0 * c, "ry_deg": -0.5, "rz_deg": 0.25,
+                             "tx_mm": 2.0, "ty_mm": -1.0, "tz_mm": 0.5},
+            best_estimate_deg_mm=None, ncc_before=ncc_b, ncc_after=ncc_a,
+            dsc_before=before, dsc_after=after,
+            aggregates=_aggregates(ncc_b, ncc_a, before, after), trace=None,
+            wall_time_s=0.125 * c, case_id=f"case{c:02d}")
+        reports.append(rep)
+    rows = percentile_summary(reports)
+    path_csv = os.path.join(OUT, "report_summary.csv")
+    write_summary_csv(rows, path_csv)
+    paths = []
+    for rep in reports:
+        p = os.path.join("/tmp", f"er_report_{rep.case_id}.json")
+        rep.save(p)
+        paths.append(open(p).read())
+    with open(os.path.join(OUT, "report_cases.json"), "w") as fh:
+        json.dump({"reports": [r.to_dict() for r in reports], "saved": paths,
+                   "summary": rows}, fh, indent=1)
+    print("report_cases.json", len(reports))
+
+
+def exhaustive_sequence_cases():
+    """exhaustive_sequence (pipeline.py:219-266) on a small 4D case, image and
+    mask mode, through the reference's numba backend."""
+    import json
+
+    from echoreg.pipeline import exhaustive_sequence
+
+    spec = PhantomSpec(dims=(20, 18, 22), frames=3, outer_semiaxes=(7.5, 6.5, 8.5),
+                       inner_semiaxes=(5.0, 4.0, 5.5), speckle_sigma=0.2, seed=9)
+    seq, masks = make_phantom(spec)
+    truth = RigidParams(0.0, math.radians(2.0), 0.0, 1.0, -1.0, 0.5)
+    case = make_pair(seq, masks, truth)
+    grid = GridSpec(half_counts=(0, 1, 0, 1, 1, 1), step_t=0.5, step_r=2.0)
+    out = {"target": np.stack([f.data for f in case.target.frames]),
+           "source": np.stack([f.data for f in case.source.frames]),
+           "target_masks": np.stack([m.data for m in case.target_masks]).astype(np.uint8),
+           "source_masks": np.stack([m.data for m in case.source_masks]).astype(np.uint8),
+           "spacing": np.array(spec.spacing)}
+    reps = {}
+    for mode in ("image", "mask"):
+        rep = exhaustive_sequence(case.target, case.source, case.target_masks,
+                                  case.source_masks, grid, mode=mode,
+                                  executor=Executor(workers=8), case_id=f"ex_{mode}")
+        d = rep.to_dict()
+        d.pop("wall_time_s")
+        reps[mode] = d
+    np.savez_compressed(os.path.join(OUT, "exhaustive_sequence.npz"), **out)
+    with open(os.path.join(OUT, "exhaustive_sequence.json"), "w") as fh:
+        json.dump({"grid": {"half_counts": list(grid.half_counts), "step_t": grid.step_t,
+                            "step_r": grid.step_r}, "reports": reps}, fh, indent=1)
+    print("exhaustive_sequence", {m: r["estimate_deg_mm"] for m, r in reps.items()})
+
+
 if __name__ == "__main__":
     print("reference echoreg", echoreg.__version__, "numpy", np.__version__)
     which = sys.argv[1:] or ["kernels", "rng", "geometry", "smc", "exhaustive",
-                             "phantom", "pipeline"]
+                             "phantom", "pipeline", "zscore", "report", "exhaustive_sequence"]
     for w in which:
         globals()[f"{w}_cases"]()
     with open(os.path.join(OUT, "SHA256SUMS"), "w") as fh:
