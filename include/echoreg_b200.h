@@ -192,7 +192,8 @@ int er_grid_to_affine(int64_t first, int64_t count, const int32_t half_counts[6]
                       double *states_dev, double *A_dev, double *b_dev, void *stream);
 
 /* First-max argmax over z_dev[0..n) folded into a running best with a strict
- * '>' (exhaustive.py:106-109): best_dev = {value f64, index i64 (as f64 bits)}. */
+ * '>' (exhaustive.py:106-109): best_dev = {value, index}, both stored as f64 (the index
+ * as its numeric value, exact below 2^53). */
 int er_argmax_update(const double *z_dev, int64_t n, int64_t base_index, double *best_dev,
                      void *stream);
 

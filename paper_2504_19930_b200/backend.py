@@ -11,6 +11,7 @@ parallelism is ``torch.distributed`` ranks (one process per GPU), see
 
 from __future__ import annotations
 
+import logging
 import os
 from dataclasses import dataclass
 
@@ -26,10 +27,24 @@ BACKEND_ENV = "ECHOREG_BACKEND"
 _ACCEPTED = ("auto", "sm100")
 
 
+_REFERENCE_CPU_BACKENDS = ("numba", "numpy")
+log = logging.getLogger("echoreg_b200")
+
+
 def get_backend(name: str | None = None):
     """Resolve the kernel module (backend.py:33-53).  Only the sm_100a module
-    exists; asking for the reference's CPU backends is a configuration error."""
-    requested = (name or os.environ.get(BACKEND_ENV) or "auto").lower()
+    exists.  An explicit request for anything else is a configuration error;
+    the reference's CPU backend names arriving through $ECHOREG_BACKEND (a
+    reference user's environment) are logged and served by sm100, so a
+    drop-in swap does not break every default Executor()."""
+    if name is not None:
+        requested = name.lower()
+    else:
+        requested = (os.environ.get(BACKEND_ENV) or "auto").lower()
+        if requested in _REFERENCE_CPU_BACKENDS:
+            log.warning("%s=%s names a reference CPU backend; this build runs the "
+                        "sm100 kernels (there is no CPU path)", BACKEND_ENV, requested)
+            requested = "sm100"
     if requested not in _ACCEPTED:
         raise BadConfig(
             f"unknown backend {requested!r}; this build provides only 'sm100' "

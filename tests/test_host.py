@@ -92,3 +92,32 @@ def test_u8_codec_volume_semantics():
 def test_rigid_params_rejects_nonfinite():
     with pytest.raises(ValueError):
         RigidParams(rx=math.nan)
+
+
+def test_backend_env_from_a_reference_setup_is_served_by_sm100(monkeypatch, caplog):
+    """$ECHOREG_BACKEND=numba/numpy (the reference's CPU backends) must not break
+    a default Executor(): logged and served by sm100.  An explicit backend=
+    argument naming them is still a configuration error."""
+    import logging
+
+    from paper_2504_19930_b200 import BadConfig
+    from paper_2504_19930_b200 import backend as bk
+
+    for name in ("numba", "numpy", "NUMBA"):
+        monkeypatch.setenv("ECHOREG_BACKEND", name)
+        with caplog.at_level(logging.WARNING, logger="echoreg_b200"):
+            assert bk.get_backend() is bk.kernels_sm100
+        assert "sm100" in caplog.text
+        with pytest.raises(BadConfig):
+            bk.get_backend(name.lower())
+    monkeypatch.setenv("ECHOREG_BACKEND", "cuda-something")
+    with pytest.raises(BadConfig):
+        bk.get_backend()
+
+
+def test_seed_beyond_64_bits_is_rejected():
+    from paper_2504_19930_b200 import BadConfig, SmcConfig
+
+    SmcConfig(seed=2 ** 64 - 1).validate()
+    with pytest.raises(BadConfig):
+        SmcConfig(seed=2 ** 64).validate()
