@@ -41,7 +41,7 @@ int main(void) {
   void *vol, *oct, *mom, *A, *B, *ncc, *deg, *nin, *ws;
   if (cudaMalloc(&vol, n) != cudaSuccess) return 1;
   cudaMemcpy(vol, host, n, cudaMemcpyHostToDevice);
-  er_volume v = {vol, ER_U8, NX, NY, NZ, 1.0 / sd, -mean / sd, NULL, NULL};
+  er_volume v = {vol, ER_U8, NX, NY, NZ, 1.0 / sd, -mean / sd, NULL, NULL, NULL};
 
   cudaMalloc(&mom, ER_MOMENTS_DOUBLES * sizeof(double));
   CHECK(er_volume_moments(&v, (double*)mom, NULL));

@@ -50,6 +50,7 @@ typedef struct er_volume {
   double alpha, gamma;  /* value = alpha * stored + gamma */
   const void *oct_dev;  /* optional er_build_oct() re-layout of a u8 volume, or NULL */
   const void *bitoct_dev; /* optional er_build_bitoct() re-layout of a binary volume */
+  const void *quad_dev;   /* optional er_build_quad() re-layout of an f32/f64 volume */
 } er_volume;
 
 int er_abi_version(void);
@@ -93,6 +94,18 @@ int er_build_oct(const er_volume *v, void *oct_dev, void *stream);
  * the mask fast path (1-byte gathers; uniform cells skip the lerps). */
 size_t er_bitoct_bytes(const er_volume *v);
 int er_build_bitoct(const er_volume *v, void *bitoct_dev, void *stream);
+
+/* Quad re-layout of an f32- or f64-stored volume for the fp32-lerp fast path:
+ * column (ci, cj) of the padded grid, ci in [0, nx], cj in [0, ny], holds
+ * nz + 2 float4 entries, entry m = the 4 corners (x[i0][j0], x[i0][j1],
+ * x[i1][j0], x[i1][j1]) of plane clamp(m - 1) with i0 = clamp(ci - 1),
+ * i1 = clamp(ci) (likewise j): the sample of padded cell (ci, cj, ck) reads
+ * entries ck and ck + 1 (two adjacent 16-byte loads).  f64 values are
+ * rounded to fp32.  er_quad_bytes() = (nx+1)(ny+1)(nz+2) * 16.  Set
+ * er_volume.quad_dev to use it in ER_LERP_F32 (with the fp64 refinement of
+ * ill-conditioned particles, as for the 8-bit path). */
+size_t er_quad_bytes(const er_volume *v);
+int er_build_quad(const er_volume *v, void *quad_dev, void *stream);
 
 /* 256-bin histogram of a u8 volume (exact int64 counts, order-free integer
  * atomics): the z-score of volume.py:119-130 on 8-bit data is computed from

@@ -44,6 +44,7 @@ class ErVolume(ctypes.Structure):
         ("gamma", _f64),
         ("oct_dev", _p),
         ("bitoct_dev", _p),
+        ("quad_dev", _p),
     ]
 
 
@@ -89,6 +90,8 @@ SIGNATURES = {
     "er_smc_update": (ctypes.c_int, [_p, _p, _p, _p, _p, _p, _p, _i64, _f64, _f64, _u64,
                                      _i64, _i32, _p, _p, _p]),
     "er_probe_read": (ctypes.c_int, [_p, _i64, _i32, _p, _p]),
+    "er_quad_bytes": (ctypes.c_size_t, [_VP]),
+    "er_build_quad": (ctypes.c_int, [_VP, _p, _p]),
     "er_smc_update_gathered": (ctypes.c_int, [_p, _i64, _i64, _p, _p, _p, _p, _p, _i64, _f64,
                                               _f64, _u64, _i64, _i32, _p, _p, _p]),
     "er_resample": (ctypes.c_int, [_VP, _d9, _d3, _i32, _i32, _i32, _p, _p]),
@@ -107,7 +110,7 @@ _lib = None
 LAUNCHES_PER_CALL = {
     "er_volume_moments": 2, "er_classify_f64": 2, "er_build_oct": 1, "er_build_bitoct": 1, "er_histogram_u8": 2, "er_convert_f64": 1, "er_minmax_f64": 3, "er_lattice_u8": 2, "er_ingest_u8": 2, "er_measure_ncc": 2,
     "er_smc_init": 1, "er_smc_predict": 1, "er_smc_predict_affine": 1, "er_states_to_affine": 1, "er_grid_to_affine": 1,
-    "er_argmax_update": 1, "er_smc_update": 1, "er_smc_update_gathered": 1, "er_probe_read": 1, "er_resample": 1, "er_warp_dice_counts": 2,
+    "er_argmax_update": 1, "er_smc_update": 1, "er_smc_update_gathered": 1, "er_probe_read": 1, "er_build_quad": 1, "er_resample": 1, "er_warp_dice_counts": 2,
     "er_warp_ncc_sums": 4, "er_phantom_speckle": 5, "er_phantom_frame": 1, "er_quantize_u8": 1,
     "er_binarize_u8": 1,
 }

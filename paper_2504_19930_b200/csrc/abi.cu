@@ -19,7 +19,8 @@ int er_set_cuda_error(cudaError_t e, const char* where) {
   return ER_ECUDA;
 }
 
-extern "C" int er_abi_version(void) { return 1; }
+// 2: er_volume gained quad_dev (round 2)
+extern "C" int er_abi_version(void) { return 2; }
 
 extern "C" const char* er_last_error(void) { return g_last_error; }
 

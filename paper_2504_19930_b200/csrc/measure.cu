@@ -616,7 +616,8 @@ struct OctGeom {
 
 
 // BITS = 1: `oct` points at the bit-oct layout of a binary source (1 byte per
-// cell).  OVL = 1: the overlap region (sum y^2 over the in-bounds voxels is
+// cell); BITS = 2: at the quad layout of an f32/f64-stored source (two
+// adjacent float4 per sample, er_build_quad).  OVL = 1: the overlap region (sum y^2 over the in-bounds voxels is
 // accumulated; the full region takes it from the target moments).
 template <typename TT, int LERP, int BITS, int OVL>
 __global__ void __launch_bounds__(OctThreads<LERP>::n,
@@ -670,8 +671,10 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   __shared__ int next_group;
   constexpr int kOctThreads = OctThreads<LERP>::n;
   constexpr int kOctWarps = OctThreads<LERP>::warps;
-  constexpr bool kSmemAcc = ER_OCT_SMEM_ACC && (kF32 || BITS);
-  constexpr bool kTgtRowFold = Acc::kRowFold && (kF32 || BITS);
+  constexpr bool kBits = BITS == 1, kQuad = BITS == 2;
+  static_assert(!kQuad || LERP == ER_LERP_F32, "the quad layout serves the fp32-lerp mode");
+  constexpr bool kSmemAcc = ER_OCT_SMEM_ACC && (kF32 || kBits);
+  constexpr bool kTgtRowFold = Acc::kRowFold && (kF32 || kBits);
   __shared__ RowRec rrec[kOctWarps][32];
   __shared__ double3 racc[kSmemAcc ? kOctThreads : 1];
   // fp64 row folds of the target terms of fp32/fp64-stored targets
@@ -805,7 +808,31 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
         // 32-bit cell index: the padded grid has < 2^31 cells
         const int cell = F::ipart(cu) * cyz + F::ipart(cv) * og.cz + F::ipart(cw);
         const TT* tp = tgt + (unsigned)er_idx(toff + k, ntv);
-        if (BITS) {
+        if (kQuad) {
+          // f32/f64-stored source: entries cell (plane k0) and cell + 1
+          // (plane k1), each (x[i0][j0], x[i0][j1], x[i1][j0], x[i1][j1])
+          const float4* q = reinterpret_cast<const float4*>(oct) +
+                            (unsigned)er_idx(cell, ncells - 1);
+          const float4 q0 = __ldg(q), q1 = __ldg(q + 1);
+          const auto yv = ty.add(__ldg(tp));
+          const float2 fuv = __fmul2_rn(make_float2(ER_U2F((unsigned)cu), ER_U2F((unsigned)cv)),
+                                        make_float2(2.3283064365386963e-10f,
+                                                    2.3283064365386963e-10f));
+          const float fw = F::frac32(cw);
+          const float2 fu2 = make_float2(fuv.x, fuv.x);
+          // u-lerps packed over j: (c00, c10) on plane k0, (c01, c11) on k1
+          const float2 a0 = make_float2(q0.x, q0.y), a1 = make_float2(q1.x, q1.y);
+          const float2 p0 = __ffma2_rn(fu2, f2sub(make_float2(q0.z, q0.w), a0), a0);
+          const float2 p1 = __ffma2_rn(fu2, f2sub(make_float2(q1.z, q1.w), a1), a1);
+          const float c0 = fmaf(fuv.y, p0.y - p0.x, p0.x);
+          const float c1 = fmaf(fuv.y, p1.y - p1.x, p1.x);
+          acc_voxel(fmaf(fw, c1 - c0, c0), (float)yv, px, pxx, pyx);
+          cu += du1;
+          cv += dv1;
+          cw += dw1;
+          continue;
+        }
+        if (kBits) {
           // binary source: one byte = the cell's 8 corner bits
           const unsigned c = __ldg(reinterpret_cast<const uint8_t*>(oct) +
                                    (unsigned)er_idx(cell, ncells));
@@ -912,7 +939,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
         cv += dv1;
         cw += dw1;
       }
-      if (kF32 || BITS) {  // fp32 row partials (<= nz/kLanes voxels) -> fp64
+      if (kF32 || kBits) {  // fp32 row partials (<= nz/kLanes voxels) -> fp64
         if (kSmemAcc) {
           double3 a = racc[threadIdx.x];
           a.x += (double)px;
@@ -938,7 +965,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
       qxx = a.y;
       qyx = a.z;
     }
-    if (BITS && ER_BITS_EXACT) {  // exact integer terms of the uniform-1 voxels
+    if (kBits && ER_BITS_EXACT) {  // exact integer terms of the uniform-1 voxels
       qx += (double)ones;
       qxx += (double)ones;
       qyx += (double)ones_y;
@@ -1009,6 +1036,28 @@ __global__ void build_bitoct_kernel(const uint8_t* __restrict__ s, int sx, int s
     out[q] = (uint8_t)(at(i0, j0, k0) | (at(i1, j0, k0) << 1) | (at(i0, j1, k0) << 2) |
                        (at(i1, j1, k0) << 3) | (at(i0, j0, k1) << 4) | (at(i1, j0, k1) << 5) |
                        (at(i0, j1, k1) << 6) | (at(i1, j1, k1) << 7));
+  }
+}
+
+// Quad re-layout of an f32/f64 source (one thread per column entry; see
+// er_build_quad in the header): entry (ci, cj, m) = the four (i, j) corners of
+// plane clamp(m - 1), values rounded to fp32.
+template <typename ST>
+__global__ void build_quad_kernel(const ST* __restrict__ s, int sx, int sy, int sz,
+                                  float4* __restrict__ out) {
+  const int cy = sy + 1, cz = sz + 2;
+  const long long n = (long long)(sx + 1) * cy * cz;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(q % cz);
+    const long long rest = q / cz;
+    const int cj = (int)(rest % cy);
+    const int ci = (int)(rest / cy);
+    const int i0 = min(max(ci - 1, 0), sx - 1), i1 = min(ci, sx - 1);
+    const int j0 = min(max(cj - 1, 0), sy - 1), j1 = min(cj, sy - 1);
+    const int k = min(max(m - 1, 0), sz - 1);
+    auto at = [&](int i, int j) -> float { return (float)s[((long long)i * sy + j) * sz + k]; };
+    out[q] = make_float4(at(i0, j0), at(i0, j1), at(i1, j0), at(i1, j1));
   }
 }
 
@@ -1269,7 +1318,30 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
   const bool use_bits =
       fast && (lerp_mode == ER_LERP_F32 || lerp_mode == ER_LERP_NEAREST) && src->bitoct_dev;
   const bool use_oct = fast && !use_bits && src->oct_dev;
-  if (use_bits || use_oct) {
+  const long long qcells = (long long)(src->nx + 1) * (src->ny + 1) * (src->nz + 2);
+  const bool use_quad = lerp_mode == ER_LERP_F32 && tgt->ny <= kRowsPerTile &&
+                        (src->dtype == ER_F32 || src->dtype == ER_F64) && src->quad_dev &&
+                        qcells < (1LL << 31);
+  if (use_quad) {
+    const OctGeom og{src->ny + 1, src->nz + 2, (long long)P};
+    const unsigned blocks = (unsigned)(P * g.ntiles);
+    const uint2* lay = (const uint2*)src->quad_dev;
+#define ER_QUAD(TT)                                                                            \
+  do {                                                                                         \
+    if (overlap_only)                                                                          \
+      measure_oct_kernel<TT, ER_LERP_F32, 2, 1><<<blocks, OctThreads<ER_LERP_F32>::n, 0, st>>>( \
+          (const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part);                           \
+    else                                                                                       \
+      measure_oct_kernel<TT, ER_LERP_F32, 2, 0><<<blocks, OctThreads<ER_LERP_F32>::n, 0, st>>>( \
+          (const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part);                           \
+  } while (0)
+    switch (tgt->dtype) {
+      case ER_U8: ER_QUAD(uint8_t); break;
+      case ER_F32: ER_QUAD(float); break;
+      default: ER_QUAD(double); break;
+    }
+#undef ER_QUAD
+  } else if (use_bits || use_oct) {
     const OctGeom og{src->ny + 1, src->nz + 1, (long long)P};
     const unsigned blocks = (unsigned)(P * g.ntiles);
     const uint2* lay = (const uint2*)(use_bits ? src->bitoct_dev : src->oct_dev);
@@ -1324,7 +1396,8 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
   // are refined where they cannot resolve 1e-4 (measure_finalize_kernel);
   // the bit-oct path samples exactly, nearest is a different operator, and
   // f64-stored sources lerp in fp64 anyway
-  const bool refine = ER_REFINE && lerp_mode == ER_LERP_F32 && !use_bits && src->dtype != ER_F64;
+  const bool refine =
+      ER_REFINE && lerp_mode == ER_LERP_F32 && !use_bits && (src->dtype != ER_F64 || use_quad);
   RefineArgs r{nullptr, nullptr, tgt->dtype != ER_U8};
   if (refine) {
     char* base = (char*)workspace_dev + partials_bytes(g, P);
@@ -1349,11 +1422,17 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
         case ER_F32: ER_REFINE_LAUNCH(float, uint8_t); break;
         default: ER_REFINE_LAUNCH(double, uint8_t); break;
       }
-    } else {
+    } else if (src->dtype == ER_F32) {
       switch (tgt->dtype) {
         case ER_U8: ER_REFINE_LAUNCH(uint8_t, float); break;
         case ER_F32: ER_REFINE_LAUNCH(float, float); break;
         default: ER_REFINE_LAUNCH(double, float); break;
+      }
+    } else {
+      switch (tgt->dtype) {
+        case ER_U8: ER_REFINE_LAUNCH(uint8_t, double); break;
+        case ER_F32: ER_REFINE_LAUNCH(float, double); break;
+        default: ER_REFINE_LAUNCH(double, double); break;
       }
     }
 #undef ER_REFINE_LAUNCH
@@ -1381,6 +1460,27 @@ extern "C" int er_build_oct(const er_volume* v, void* oct_dev, void* stream) {
   if (blocks > ER_NUM_SMS_B200 * 16) blocks = ER_NUM_SMS_B200 * 16;
   build_oct_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
       (const uint8_t*)v->data_dev, v->nx, v->ny, v->nz, (uint2*)oct_dev);
+  ER_CHECK_LAUNCH();
+  return ER_OK;
+}
+
+extern "C" size_t er_quad_bytes(const er_volume* v) {
+  if (!v || v->nx < 1 || v->ny < 1 || v->nz < 1) return 0;
+  return (size_t)(v->nx + 1) * (size_t)(v->ny + 1) * (size_t)(v->nz + 2) * sizeof(float4);
+}
+
+extern "C" int er_build_quad(const er_volume* v, void* quad_dev, void* stream) {
+  if (!valid_volume(v) || (v->dtype != ER_F32 && v->dtype != ER_F64) || !quad_dev)
+    return er_set_error(ER_EINVAL, "er_build_quad: needs an f32/f64 volume and an output buffer");
+  const long long n = (long long)(v->nx + 1) * (v->ny + 1) * (v->nz + 2);
+  long long blocks = (n + 255) / 256;
+  if (blocks > ER_NUM_SMS_B200 * 16) blocks = ER_NUM_SMS_B200 * 16;
+  if (v->dtype == ER_F32)
+    build_quad_kernel<float><<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+        (const float*)v->data_dev, v->nx, v->ny, v->nz, (float4*)quad_dev);
+  else
+    build_quad_kernel<double><<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+        (const double*)v->data_dev, v->nx, v->ny, v->nz, (float4*)quad_dev);
   ER_CHECK_LAUNCH();
   return ER_OK;
 }

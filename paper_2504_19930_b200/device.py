@@ -138,12 +138,33 @@ class DeviceVolume:
                 self.bitoct = lay
         self.desc.bitoct_dev = lay.data_ptr()
 
-    def ensure_fast_layout(self):
-        """The measurement fast-path layout for this source: bit-oct for
-        binary 8-bit data, oct for other 8-bit data."""
-        if self.dtype_code != _lib.ER_U8:
+    def quad_fits(self) -> bool:
+        nx, ny, nz = self.dims
+        return (nx + 1) * (ny + 1) * (nz + 2) < 2**31
+
+    def ensure_quad(self):
+        """Build (once) the quad re-layout of an f32/f64-stored source (the
+        fp32-lerp fast path for non-8-bit data: two adjacent 16-byte loads per
+        sample instead of eight scalar gathers)."""
+        if self.dtype_code not in (_lib.ER_F32, _lib.ER_F64) or self.desc.quad_dev \
+                or not self.quad_fits():
             return
-        if self.stored_binary():
+        lay = getattr(self, "quad", None)
+        if lay is None:
+            t = torch()
+            nbytes = int(_lib.load().er_quad_bytes(ctypes.byref(self.desc)))
+            lay = t.empty(nbytes, dtype=t.uint8, device=self.storage.device)
+            _lib.call("er_build_quad", ctypes.byref(self.desc), ptr(lay),
+                      stream_ptr(self.storage.device))
+            self.quad = lay
+        self.desc.quad_dev = lay.data_ptr()
+
+    def ensure_fast_layout(self):
+        """The fp32-lerp fast-path layout for this source: bit-oct for binary
+        8-bit data, oct for other 8-bit data, quad for f32/f64 storage."""
+        if self.dtype_code != _lib.ER_U8:
+            self.ensure_quad()
+        elif self.stored_binary():
             self.ensure_bitoct()
         else:
             self.ensure_oct()

@@ -69,9 +69,10 @@ def measure(tdv: DeviceVolume, sdv: DeviceVolume, A, B, overlap: bool, precision
 
 def refines(sdv: DeviceVolume, precision: str) -> bool:
     """Whether er_measure_ncc runs its fp64 refinement pass for this source
-    (fp32 lerps on a non-binary u8 or an f32-stored source)."""
-    return (precision == "f32" and sdv.dtype_code != _lib.ER_F64
-            and not sdv.desc.bitoct_dev)
+    (fp32 lerps on a non-binary u8 source, an f32-stored source, or an
+    f64-stored source through its quad layout)."""
+    return (precision == "f32" and not sdv.desc.bitoct_dev
+            and (sdv.dtype_code != _lib.ER_F64 or bool(sdv.desc.quad_dev)))
 
 
 def _as_dv(v, device=None) -> DeviceVolume:

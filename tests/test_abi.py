@@ -38,15 +38,15 @@ def test_binding_covers_header():
 
 
 def test_struct_layouts_match_header():
-    # er_volume: ptr, 4 x int32, 2 x double, 2 x ptr -> 56 bytes on LP64
-    assert ctypes.sizeof(_lib.ErVolume) == 56
+    # er_volume: ptr, 4 x int32, 2 x double, 3 x ptr -> 64 bytes on LP64
+    assert ctypes.sizeof(_lib.ErVolume) == 64
     # er_smc_ctl: 7 doubles + 2 int32
     assert ctypes.sizeof(_lib.ErSmcCtl) == 64
 
 
 def test_abi_version_and_error_text_without_gpu():
     lib = _lib.load()
-    assert lib.er_abi_version() == 1
+    assert lib.er_abi_version() == 2
     assert isinstance(lib.er_last_error(), bytes)
 
 
