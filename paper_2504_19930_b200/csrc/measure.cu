@@ -91,6 +91,13 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_OCT_LANES
 #define ER_OCT_LANES (ER_OCT_HALF ? 8 : 32)
 #endif
+#ifndef ER_OPAQUE_STEP
+#define ER_OPAQUE_STEP 0
+#endif
+// two of the eight corner conversions of the pair loop on the XU pipe
+#ifndef ER_CORNER_XU
+#define ER_CORNER_XU 1
+#endif
 // 8-bit target values to float on the XU pipe (I2F.U8) instead of the ALU (I2FP)
 #ifndef ER_TGT_XU
 #define ER_TGT_XU 1
@@ -462,6 +469,13 @@ __device__ __forceinline__ float byte_magic(unsigned w, unsigned sel) {
   return __int_as_float(__byte_perm(w, 0x4B000000u, sel | 0x7650u));
 }
 
+// byte b of w as a float on the XU pipe (I2F.U8 with a byte selector)
+__device__ __forceinline__ float u8sel_f(unsigned w, int b) {
+  float r;
+  asm("cvt.rn.f32.u8 %0, %1;" : "=f"(r) : "h"((unsigned short)(w >> (8 * b))));
+  return r;
+}
+
 // 2^52 + byte as an exact double (no offset removed)
 __device__ __forceinline__ double byte_m64(unsigned w, unsigned sel) {
   return __hiloint2double(0x43300000, __byte_perm(w, 0u, sel | 0x4440u));
@@ -587,15 +601,27 @@ __device__ __forceinline__ float lerp_oct_f32(uint2 c8, float fu, float fv, floa
 __device__ __forceinline__ float2 lerp_oct_f32x2(uint2 a8, uint2 b8, float2 fu, float2 fv,
                                                  float2 fw) {
   const float2 off2 = make_float2(-8388608.0f, -8388608.0f);
+#if ER_CORNER_XU
+  // the (x000, x100) pair converted on the XU pipe (I2F.U8 with a byte
+  // selector, exact values, no offset), the other six corners by PRMT on the
+  // ALU pipe: balances the two pipes
+  const float2 x000 = make_float2(u8sel_f(a8.x, 0), u8sel_f(b8.x, 0));
+  const float2 x100 = make_float2(u8sel_f(a8.x, 1), u8sel_f(b8.x, 1));
+#else
   const float2 x000 = make_float2(byte_magic(a8.x, 0), byte_magic(b8.x, 0));
   const float2 x100 = make_float2(byte_magic(a8.x, 1), byte_magic(b8.x, 1));
+#endif
   const float2 x010 = make_float2(byte_magic(a8.x, 2), byte_magic(b8.x, 2));
   const float2 x110 = make_float2(byte_magic(a8.x, 3), byte_magic(b8.x, 3));
   const float2 x001 = make_float2(byte_magic(a8.y, 0), byte_magic(b8.y, 0));
   const float2 x101 = make_float2(byte_magic(a8.y, 1), byte_magic(b8.y, 1));
   const float2 x011 = make_float2(byte_magic(a8.y, 2), byte_magic(b8.y, 2));
   const float2 x111 = make_float2(byte_magic(a8.y, 3), byte_magic(b8.y, 3));
+#if ER_CORNER_XU
+  const float2 c00 = __ffma2_rn(fu, f2sub(x100, x000), x000);
+#else
   const float2 c00 = __ffma2_rn(fu, f2sub(x100, x000), __fadd2_rn(x000, off2));
+#endif
   const float2 c10 = __ffma2_rn(fu, f2sub(x110, x010), __fadd2_rn(x010, off2));
   const float2 c01 = __ffma2_rn(fu, f2sub(x101, x001), __fadd2_rn(x001, off2));
   const float2 c11 = __ffma2_rn(fu, f2sub(x111, x011), __fadd2_rn(x011, off2));
@@ -692,7 +718,14 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   // fp32 byte path: voxels k and k + kLanes of a lane are sampled together
   constexpr bool kPair = ER_OCT_PAIR && LERP == ER_LERP_F32 && !BITS;
   const long long du1 = kLanes * du, dv1 = kLanes * dv, dw1 = kLanes * dw;
-  const long long du2 = 2 * du1, dv2 = 2 * dv1, dw2 = 2 * dw1;
+  long long du2 = 2 * du1, dv2 = 2 * dv1, dw2 = 2 * dw1;
+#if ER_OPAQUE_STEP
+  // keep the per-iteration steps in registers (else ptxas re-derives them
+  // from du with LEA shift-adds on the ALU pipe)
+  asm volatile("mov.b64 %0, %0;" : "+l"(du2));
+  asm volatile("mov.b64 %0, %0;" : "+l"(dv2));
+  asm volatile("mov.b64 %0, %0;" : "+l"(dw2));
+#endif
 
   for (int grp = warp; grp < ngroups;) {
     const int r = grp * 32 + lane;
