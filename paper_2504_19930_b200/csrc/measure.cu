@@ -87,6 +87,10 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_REFINE
 #define ER_REFINE 1
 #endif
+// fp64-lerp byte path: Q12.52 coordinates + pair loop where the affine allows
+#ifndef ER_F64_Q52
+#define ER_F64_Q52 1
+#endif
 // lanes per target row in the oct kernels (8, 16 or 32; rows per warp = 32 / lanes)
 #ifndef ER_OCT_LANES
 #define ER_OCT_LANES (ER_OCT_HALF ? 8 : 32)
@@ -630,6 +634,44 @@ __device__ __forceinline__ float2 lerp_oct_f32x2(uint2 a8, uint2 b8, float2 fu, 
   return __ffma2_rn(fw, f2sub(c1, c0), c0);
 }
 
+// Q12.52 coordinates of the fp64-lerp byte path (kQ52Path)
+__device__ __forceinline__ int q52_ipart(long long q) { return (int)(q >> 52); }
+
+// The fractional part of a Q12.52 coordinate as an exact double: its 52
+// fraction bits become the mantissa of 1 + f (one LOP3 on the high word).
+__device__ __forceinline__ double q52_frac(long long q) {
+  return __hiloint2double((int)((((unsigned)((unsigned long long)q >> 32)) & 0xFFFFFu) |
+                                0x3FF00000u),
+                          (int)(unsigned)q) - 1.0;
+}
+
+// 2^52 + byte * 2^40 as an exact double: the byte goes into bits 8..15 of
+// the high word (one PRMT), the low word is 0.
+__device__ __forceinline__ double byte_hi52(unsigned w, unsigned sel) {
+  return __hiloint2double((int)__byte_perm(w, 0x43300000u, 0x7604u | (sel << 4)), 0);
+}
+
+// fp64 trilinear sample of one oct cell from Q12.52 coordinates, in units of
+// 2^-40 (the corners are 2^52 + byte * 2^40, integers below 2^53).  The whole
+// lerp chain runs on the 2^52-offset values: every difference cancels the
+// offset exactly, every lerp result is 2^52 + value rounded to one unit
+// (2^-41 byte), and the offset is removed once at the end -- one DADD instead
+// of one per base corner.
+__device__ __forceinline__ double lerp_q52(uint2 c8, long long cu, long long cv, long long cw) {
+  const double fu = q52_frac(cu), fv = q52_frac(cv), fw = q52_frac(cw);
+  const double m000 = byte_hi52(c8.x, 0), m100 = byte_hi52(c8.x, 1);
+  const double m010 = byte_hi52(c8.x, 2), m110 = byte_hi52(c8.x, 3);
+  const double m001 = byte_hi52(c8.y, 0), m101 = byte_hi52(c8.y, 1);
+  const double m011 = byte_hi52(c8.y, 2), m111 = byte_hi52(c8.y, 3);
+  const double c00 = fma(fu, m100 - m000, m000);
+  const double c10 = fma(fu, m110 - m010, m010);
+  const double c01 = fma(fu, m101 - m001, m001);
+  const double c11 = fma(fu, m111 - m011, m011);
+  const double c0 = fma(fv, c10 - c00, c00);
+  const double c1 = fma(fv, c11 - c01, c01);
+  return fma(fw, c1 - c0, c0) - 4503599627370496.0;
+}
+
 struct RowRec {  // one target row of a 32-row group, in fixed point
   long long fu0, fv0, fw0;
   int klo, khi, off, pad;
@@ -674,10 +716,25 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   if (threadIdx.x < 12)
     sab[threadIdx.x] = threadIdx.x < 9 ? A[9 * p + threadIdx.x] : B[3 * p + threadIdx.x - 9];
   __syncthreads();
+  // fp64-lerp byte path: Q12.52 coordinates (a fraction is one masked high
+  // word; see lerp_q52) whenever the particle's affine keeps every coordinate
+  // of the tile inside +-2^11 voxels -- a uniform per-CTA guard; else Q24.40
+  constexpr bool kQ52Path = ER_F64_Q52 && LERP == ER_LERP_F64 && BITS == 0;
+  bool q52 = false;
+  if (kQ52Path) {
+    const double mu = fabs(sab[9]) + fabs(sab[0]) * g.nx + fabs(sab[1]) * g.ny +
+                      fabs(sab[2]) * g.nz;
+    const double mv = fabs(sab[10]) + fabs(sab[3]) * g.nx + fabs(sab[4]) * g.ny +
+                      fabs(sab[5]) * g.nz;
+    const double mw = fabs(sab[11]) + fabs(sab[6]) * g.nx + fabs(sab[7]) * g.ny +
+                      fabs(sab[8]) * g.nz;
+    q52 = fmax(mu, fmax(mv, mw)) < 2000.0;
+  }
+  const double kscale = q52 ? 4503599627370496.0 : F::kScale;  // 2^52 or 2^FB
   // fixed-point per-k increments (exact integer stepping along the row)
-  const long long du = __double2ll_rn(sab[2] * F::kScale);
-  const long long dv = __double2ll_rn(sab[5] * F::kScale);
-  const long long dw = __double2ll_rn(sab[8] * F::kScale);
+  const long long du = __double2ll_rn(sab[2] * kscale);
+  const long long dv = __double2ll_rn(sab[5] * kscale);
+  const long long dw = __double2ll_rn(sab[8] * kscale);
 
   const int i_begin = tile * g.planes_per_tile;
   const int i_end = min(g.nx, i_begin + g.planes_per_tile);
@@ -758,13 +815,13 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
     // row start in fixed point (per lane: its own row)
     // (the +1.0 voxel shift to the padded cell index is an exact integer add,
     // so the cell index below is a plain non-negative 32-bit IMAD chain)
-    const long long one = 1LL << (kF32 ? 32 : 40);
+    const long long one = 1LL << (q52 ? 52 : (kF32 ? 32 : 40));
     // the lane's row record goes to shared memory (broadcast reads below), so
     // it does not occupy registers across the voxel loop
     RowRec& mine = rrec[warp][lane];
-    mine.fu0 = __double2ll_rn(u0 * F::kScale) + one;
-    mine.fv0 = __double2ll_rn(v0 * F::kScale) + one;
-    mine.fw0 = __double2ll_rn(w0 * F::kScale) + one;
+    mine.fu0 = __double2ll_rn(u0 * kscale) + one;
+    mine.fv0 = __double2ll_rn(v0 * kscale) + one;
+    mine.fw0 = __double2ll_rn(w0 * kscale) + one;
     mine.klo = klo;
     mine.khi = khi;
     mine.off = off;
@@ -792,6 +849,47 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
         cw = rq.fw0 + (long long)k0 * dw;
       }
       int k = k0;
+      if (kQ52Path && q52) {
+        // fp64 lerps in Q12.52: two voxels per lane per step (k, k + kLanes)
+        // sharing the loop test and the target address; samples carry a 2^40
+        // scale (lerp_q52), removed exactly when the group is folded
+        int ti = toff + k;
+        const int ti_end = toff + qhi - kLanes;
+        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
+        for (; ti < ti_end; ti += 2 * kLanes) {
+          const int ca = (q52_ipart(cu) * og.cy + q52_ipart(cv)) * og.cz + q52_ipart(cw);
+          const int cb = (q52_ipart(bu) * og.cy + q52_ipart(bv)) * og.cz + q52_ipart(bw);
+          const uint2 a8 = ld_oct(oct + (unsigned)er_idx(ca, ncells));
+          const uint2 b8 = ld_oct(oct + (unsigned)er_idx(cb, ncells));
+          const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
+          const double ya = (double)ty.add(__ldg(tp));
+          const double yb = (double)ty.add(__ldg(tp + kLanes));
+          const double xa = lerp_q52(a8, cu, cv, cw);
+          const double xb = lerp_q52(b8, bu, bv, bw);
+          qx += xa;
+          qxx = fma(xa, xa, qxx);
+          qyx = fma(ya, xa, qyx);
+          qx += xb;
+          qxx = fma(xb, xb, qxx);
+          qyx = fma(yb, xb, qyx);
+          cu += du2;
+          cv += dv2;
+          cw += dw2;
+          bu += du2;
+          bv += dv2;
+          bw += dw2;
+        }
+        if (ti < toff + qhi) {  // this lane's last voxel, unpaired
+          const int ca = (q52_ipart(cu) * og.cy + q52_ipart(cv)) * og.cz + q52_ipart(cw);
+          const uint2 a8 = ld_oct(oct + (unsigned)er_idx(ca, ncells));
+          const double ya = (double)ty.add(__ldg(tgt + (unsigned)er_idx(ti, ntv)));
+          const double xa = lerp_q52(a8, cu, cv, cw);
+          qx += xa;
+          qxx = fma(xa, xa, qxx);
+          qyx = fma(ya, xa, qyx);
+        }
+        k = qhi;
+      }
       if (kPair) {
         // two voxels per lane per step (k and k + kLanes): the fractions, the
         // whole lerp chain and the accumulation run as fp32x2 pairs across the
@@ -1002,6 +1100,11 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
       qx += (double)ones;
       qxx += (double)ones;
       qyx += (double)ones_y;
+    }
+    if (kQ52Path && q52) {  // lerp_q52's 2^40 sample scale, removed exactly
+      qx *= 9.094947017729282e-13;
+      qxx *= 8.271806125530277e-25;
+      qyx *= 9.094947017729282e-13;
     }
     // fold the group: fixed-order warp reduction in fp64 into the group slot
     double v[5];
