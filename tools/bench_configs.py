@@ -214,17 +214,24 @@ def scaling(p_list=(2000, 65536), n_list=(1, 2, 4, 8), reps=5):
     nvox = t.data.size
     out = []
 
-    def local_gather(local, plan, dst):  # the NCCL exchange's cost is estimated below
-        dst[: plan.count].copy_(local[: plan.count])
-        return dst[: plan.n]
+    def local_gather(local, out):  # the NCCL exchange's cost is estimated below
+        out[: local.numel()].copy_(local)
+        return out
 
-    dsmc.dist.allgather_shards = local_gather
+    dsmc.dist.allgather_packed = local_gather
     for P in p_list:
         cfg = SmcConfig(mode="image", n_particles=P, n_iterations=reps + 2, seed=0)
         base = None
         for N in n_list:
             run = dsmc.DeviceSmcRun(t, s, cfg, Executor())
             run.plan = dist.ShardPlan(P, N, 0)  # rank 0 holds the first (largest) shard
+            # rank 0's packed block [z | flags] and the gathered buffer of N blocks
+            S = run.plan.shard
+            run.block = dist.packed_block_bytes(S)
+            run.zd_local = torch.zeros(run.block, dtype=torch.uint8, device=run.dev)
+            run.z_local = run.zd_local[: 8 * S].view(torch.float64)
+            run.dg_local = run.zd_local[8 * S: 9 * S]
+            run.zd_all = torch.zeros(run.block * N, dtype=torch.uint8, device=run.dev)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             for k in range(2):
                 run.step(k)
