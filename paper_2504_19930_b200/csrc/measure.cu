@@ -91,9 +91,15 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_F64_Q52
 #define ER_F64_Q52 1
 #endif
-// lanes per target row in the oct kernels (8, 16 or 32; rows per warp = 32 / lanes)
+// lanes per target row in the oct kernels (4, 8, 16 or 32; rows per warp =
+// 32 / lanes): fewer lanes per row amortise the per-row setup over more rows
+// per warp step; 4 is the measured best for the lerp modes (2 loses the
+// coalescing), 8 for the nearest mode
 #ifndef ER_OCT_LANES
-#define ER_OCT_LANES (ER_OCT_HALF ? 8 : 32)
+#define ER_OCT_LANES (ER_OCT_HALF ? 4 : 32)
+#endif
+#ifndef ER_OCT_LANES_NEAREST
+#define ER_OCT_LANES_NEAREST (ER_OCT_HALF ? 8 : 32)
 #endif
 #ifndef ER_OPAQUE_STEP
 #define ER_OPAQUE_STEP 0
@@ -769,7 +775,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   // kLanes lanes per row: 32 (one row at a time) or 16 (two rows side by
   // side on the half-warps: for nz = 208 = 13 x 16 no lane idles at the row
   // end, and each lane's per-row overhead is paid over twice the voxels)
-  constexpr int kLanes = ER_OCT_LANES;
+  constexpr int kLanes = LERP == ER_LERP_NEAREST ? ER_OCT_LANES_NEAREST : ER_OCT_LANES;
   constexpr int kRowsPerWarp = 32 / kLanes;
   const int sub = lane & (kLanes - 1);
   // fp32 byte path: voxels k and k + kLanes of a lane are sampled together
