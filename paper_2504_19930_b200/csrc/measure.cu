@@ -824,25 +824,24 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
     const long long one = 1LL << (q52 ? 52 : (kF32 ? 32 : 40));
     // the lane's row record goes to shared memory (broadcast reads below), so
     // it does not occupy registers across the voxel loop
-    RowRec& mine = rrec[warp][lane];
-    mine.fu0 = __double2ll_rn(u0 * kscale) + one;
-    mine.fv0 = __double2ll_rn(v0 * kscale) + one;
-    mine.fw0 = __double2ll_rn(w0 * kscale) + one;
-    mine.klo = klo;
-    mine.khi = khi;
-    mine.off = off;
-    unsigned rows = __ballot_sync(0xffffffffu, khi > klo);
+    // non-empty rows only, compacted in row order: the lane's record goes to
+    // the slot of its rank among them, so each step of the row loop below
+    // takes the next kRowsPerWarp records with one shared-memory read
+    const unsigned rows = __ballot_sync(0xffffffffu, khi > klo);
+    const int nrows = __popc(rows);
+    if (khi > klo) {
+      RowRec& mine = rrec[warp][__popc(rows & ((1u << lane) - 1u))];
+      mine.fu0 = __double2ll_rn(u0 * kscale) + one;
+      mine.fv0 = __double2ll_rn(v0 * kscale) + one;
+      mine.fw0 = __double2ll_rn(w0 * kscale) + one;
+      mine.klo = klo;
+      mine.khi = khi;
+      mine.off = off;
+    }
     __syncwarp();
-    while (rows) {
-      // the next kRowsPerWarp non-empty rows, one per lane group (uniform)
-      int q = -1;
-      const int myslot = lane / kLanes;
-#pragma unroll
-      for (int s = 0; s < kRowsPerWarp; ++s) {
-        const int b = rows ? __ffs(rows) - 1 : -1;
-        if (b >= 0) rows &= rows - 1;
-        if (s == myslot) q = b;
-      }
+    const int myslot = lane / kLanes;
+    for (int base = 0; base < nrows; base += kRowsPerWarp) {
+      const int q = base + myslot < nrows ? base + myslot : -1;
       int qhi = 0, k0 = 1, toff = 0;
       long long cu = 0, cv = 0, cw = 0;
       if (q >= 0) {
