@@ -98,6 +98,9 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_OCT_LANES
 #define ER_OCT_LANES (ER_OCT_HALF ? 4 : 32)
 #endif
+#ifndef ER_OCT_LANES_F64
+#define ER_OCT_LANES_F64 ER_OCT_LANES
+#endif
 #ifndef ER_OCT_LANES_NEAREST
 #define ER_OCT_LANES_NEAREST (ER_OCT_HALF ? 8 : 32)
 #endif
@@ -775,7 +778,9 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   // kLanes lanes per row: 32 (one row at a time) or 16 (two rows side by
   // side on the half-warps: for nz = 208 = 13 x 16 no lane idles at the row
   // end, and each lane's per-row overhead is paid over twice the voxels)
-  constexpr int kLanes = LERP == ER_LERP_NEAREST ? ER_OCT_LANES_NEAREST : ER_OCT_LANES;
+  constexpr int kLanes = LERP == ER_LERP_NEAREST ? ER_OCT_LANES_NEAREST
+                        : LERP == ER_LERP_F64   ? ER_OCT_LANES_F64
+                                                : ER_OCT_LANES;
   constexpr int kRowsPerWarp = 32 / kLanes;
   const int sub = lane & (kLanes - 1);
   // fp32 byte path: voxels k and k + kLanes of a lane are sampled together
