@@ -101,6 +101,13 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_OCT_LANES_F64
 #define ER_OCT_LANES_F64 ER_OCT_LANES
 #endif
+#ifndef ER_OCT_LANES_QUAD
+#define ER_OCT_LANES_QUAD 8
+#endif
+// the fp32 byte path switches to 8 lanes per row above this oct footprint
+#ifndef ER_OCT_BIG_BYTES
+#define ER_OCT_BIG_BYTES (80LL << 20)
+#endif
 #ifndef ER_OCT_LANES_NEAREST
 #define ER_OCT_LANES_NEAREST (ER_OCT_HALF ? 8 : 32)
 #endif
@@ -696,7 +703,20 @@ struct OctGeom {
 // cell); BITS = 2: at the quad layout of an f32/f64-stored source (two
 // adjacent float4 per sample, er_build_quad).  OVL = 1: the overlap region (sum y^2 over the in-bounds voxels is
 // accumulated; the full region takes it from the target moments).
-template <typename TT, int LERP, int BITS, int OVL>
+// Lanes per target row by default (LN = 0): 4 for the lerp modes, 8 for nearest
+// and for the quad layout (two 16-byte loads per sample: fewer lanes per row
+// lose too much coalescing); the fp32 byte path is launched with 8 when the
+// oct source is too large to stay L2-resident (C5's 256^3: 136 MB).
+template <int LERP, int BITS, int LN>
+struct OctLanes {
+  static constexpr int n = LN ? LN
+                           : LERP == ER_LERP_NEAREST ? ER_OCT_LANES_NEAREST
+                           : LERP == ER_LERP_F64     ? ER_OCT_LANES_F64
+                           : BITS == 2               ? ER_OCT_LANES_QUAD
+                                                     : ER_OCT_LANES;
+};
+
+template <typename TT, int LERP, int BITS, int OVL, int LN = 0>
 __global__ void __launch_bounds__(OctThreads<LERP>::n,
                                    LERP != ER_LERP_F64 ? ER_OCT_MINBLOCKS_F32 : ER_OCT_MINBLOCKS_F64)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
@@ -778,9 +798,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   // kLanes lanes per row: 32 (one row at a time) or 16 (two rows side by
   // side on the half-warps: for nz = 208 = 13 x 16 no lane idles at the row
   // end, and each lane's per-row overhead is paid over twice the voxels)
-  constexpr int kLanes = LERP == ER_LERP_NEAREST ? ER_OCT_LANES_NEAREST
-                        : LERP == ER_LERP_F64   ? ER_OCT_LANES_F64
-                                                : ER_OCT_LANES;
+  constexpr int kLanes = OctLanes<LERP, BITS, LN>::n;
   constexpr int kRowsPerWarp = 32 / kLanes;
   const int sub = lane & (kLanes - 1);
   // fp32 byte path: voxels k and k + kLanes of a lane are sampled together
@@ -1505,12 +1523,25 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
     if (lerp_mode == ER_LERP_NEAREST) ER_OCT(TT, ER_LERP_NEAREST, 1);     \
     else ER_OCT(TT, ER_LERP_F32, 1);                                      \
   } while (0)
+#define ER_OCT_BIG(TT)                                                                     \
+  do {                                                                                     \
+    if (overlap_only)                                                                      \
+      measure_oct_kernel<TT, ER_LERP_F32, 0, 1, 8>                                         \
+          <<<blocks, OctThreads<ER_LERP_F32>::n, 0, st>>>((const TT*)tgt->data_dev, lay,   \
+                                                          A_dev, b_dev, g, og, part);      \
+    else                                                                                   \
+      measure_oct_kernel<TT, ER_LERP_F32, 0, 0, 8>                                         \
+          <<<blocks, OctThreads<ER_LERP_F32>::n, 0, st>>>((const TT*)tgt->data_dev, lay,   \
+                                                          A_dev, b_dev, g, og, part);      \
+  } while (0)
 #define ER_OCT_BYTES(TT)                                                  \
   do {                                                                    \
     if (lerp_mode == ER_LERP_NEAREST) ER_OCT(TT, ER_LERP_NEAREST, 0);     \
+    else if (lerp_mode == ER_LERP_F32 && big) ER_OCT_BIG(TT);             \
     else if (lerp_mode == ER_LERP_F32) ER_OCT(TT, ER_LERP_F32, 0);        \
     else ER_OCT(TT, ER_LERP_F64, 0);                                      \
   } while (0)
+    const bool big = cells * 8 > ER_OCT_BIG_BYTES;
     if (use_bits) {
       switch (tgt->dtype) {
         case ER_U8: ER_OCT_BITS(uint8_t); break;
@@ -1526,6 +1557,7 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
     }
 #undef ER_OCT_BITS
 #undef ER_OCT_BYTES
+#undef ER_OCT_BIG
 #undef ER_OCT
   } else {
     switch (tgt->dtype) {
