@@ -53,6 +53,13 @@ UNIT = "evals/s"
 WORKLOAD = "C2: image-mode SMC, 176x176x208 uint8 echo-like pair, 2000 particles, ED frame"
 
 
+def workload_config(particles, voxels, dims):
+    """The `config` of both arms' lines: the workload only (the same dict for
+    --impl ours and --impl reference); how an arm runs it goes under `run`."""
+    return {"workload": WORKLOAD, "particles": int(particles), "voxels": int(voxels),
+            "volume_dims": [int(d) for d in dims]}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -240,8 +247,9 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "particles": args.particles, "voxels": nvox,
-                   "volume_dims": inp["dims"], "host_threads": threads},
+        "config": workload_config(args.particles, nvox, inp["dims"]),
+        "run": {"host_threads": threads, "precision": "f64 (the reference's arithmetic)",
+                "step": "ncc_measure_batch of every particle of SMC iteration 0"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -445,11 +453,13 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32" if precision == "f32" else "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "particles": P, "voxels": nvox,
-                       "volume_dims": list(t.dims), "storage": "u8 (raw echo, z-score folded)",
-                       "precision": precision, "l2": "flushed (256 MiB write) between steps",
-                       "step": "one device SMC iteration (predict+affine+measure+update)",
-                       "parallelism": f"particles sharded over {world} GPU(s)"},
+            # the workload (identical to the reference arm's config); how this
+            # arm runs it is under "run"
+            "config": workload_config(P, nvox, t.dims),
+            "run": {"storage": "u8 (raw echo, z-score folded)",
+                    "precision": precision, "l2": "flushed (256 MiB write) between steps",
+                    "step": "one device SMC iteration (predict+affine+measure+update)",
+                    "parallelism": f"particles sharded over {world} GPU(s)"},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
             "refined_particles_last_step": refined,
             "precision_modes": modes,

@@ -933,6 +933,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
         // voxel b = voxel a + kLanes along the row: its own coordinate set,
         // both stepped by 2 kLanes per iteration
         long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
+
         for (; ti < ti_end; ti += 2 * kLanes) {
           // Horner form: two IMADs per cell index
           const int ca = (F::ipart(cu) * og.cy + F::ipart(cv)) * og.cz + F::ipart(cw);

@@ -62,3 +62,13 @@ def test_reference_arm_inputs_never_import_the_product():
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "clean" in r.stdout
+
+
+def test_both_bench_arms_quote_the_same_config():
+    """bench.py's two arms build `config` from one function on the same
+    workload numbers (the driver compares them)."""
+    import bench
+
+    a = bench.workload_config(2000, 176 * 176 * 208, (176, 176, 208))
+    b = bench.workload_config(2000, 6443008, [176, 176, 208])
+    assert a == b and a["workload"] == bench.WORKLOAD and a["particles"] == 2000
