@@ -2,27 +2,29 @@
 // likelihood per particle.  Replaces the reference's _ncc_kernel
 // (/root/reference/pkg/src/echoreg/kernels_numba.py:116-189).
 //
-// Decomposition (B200-first, see DESIGN.md "measure kernel"):
-//   * one CTA (256 threads, 8 warps) per (particle, tile of target planes);
-//     the tile shape depends only on the target dims, never on P or on the
-//     GPU count, so every particle's reduction order is fixed -> results are
+// Decomposition (B200-first, see DESIGN.md section 4):
+//   * one CTA per (particle, tile of target planes), launched tile-major; the
+//     tile shape depends only on the target dims, never on P or on the GPU
+//     count, so every particle's reduction order is fixed -> results are
 //     bitwise identical for any sharding (the reference's worker-invariance
 //     contract, kernels_numba.py:6-8).
 //   * a warp takes 32 target rows (i, j) at a time; lane r computes row r's
 //     in-bounds k-run with the reference's exact fp64 _k_interval
 //     (kernels_numba.py:88-113, 156-158) -> the in-bounds voxel set and the
-//     overlap count n are bit-exact.  The warp then walks the non-empty rows,
-//     lanes strided over k (k is the contiguous axis, volume.py:33), so target
-//     reads are coalesced and the 8 source gathers of neighbouring lanes fall
-//     in the same or adjacent cache lines.
-//   * source coordinates u = u0 + a02*k are formed in fp64 exactly as the
-//     reference does (no FMA), fractions in fp64; the 7 lerps run in fp32,
-//     fp64, or fp64 in the reference's a(1-f)+bf order (lerp_mode).
-//   * per-thread fp64 accumulation of {sum x, sum x^2, sum y*x, sum y,
-//     sum y^2} over in-bounds voxels (x = interpolated stored source value,
-//     y = stored target value), fixed-order warp-shuffle + smem block
-//     reduction, one 48-byte partial per CTA, fixed-order finalize per
-//     particle.  No float atomics anywhere.
+//     overlap count n are bit-exact.  The non-empty rows are compacted by rank
+//     and walked by a few lanes each (fast paths: 4 lanes, 8 rows per warp
+//     step), lanes strided over k (k is the contiguous axis, volume.py:33).
+//   * fast paths (measure_oct_kernel): the source re-laid out per cell (8-bit
+//     "oct": 8 corners in one 8-byte word; binary "bit-oct": 8 corner bits;
+//     f32/f64 "quad": two float4 per sample), fixed-point coordinates from the
+//     reference's fp64 row start, fp32 lerps packed fp32x2 across voxel pairs
+//     (or fp64 lerps in Q12.52 / Q24.40), fp32 row partials folded into fp64
+//     per row.  Generic path (measure_partials_kernel): 8 gathers per voxel,
+//     fp64 coordinates exactly as the reference, any storage / lerp mode.
+//   * fixed-order warp-shuffle + shared-memory reductions, one 48-byte partial
+//     per (particle, tile), fixed-order finalize per particle.  No float
+//     atomics anywhere.  fp32-lerp measurements are followed by a device-side
+//     refinement pass that re-measures ill-conditioned particles in fp64.
 //   * the value affine (value = alpha*stored + gamma, e.g. raw uint8 echo
 //     data with the z-score folded in) is applied once per particle in the
 //     finalize, so the gather moves 1 byte per corner for uint8 volumes.
@@ -30,20 +32,26 @@
 // Build-time tuning flags (ER_NVCC_EXTRA="-DNAME=V"; the defaults are the
 // measured best on the B200, the alternatives are kept for the variant
 // scripts tools/variants*.sh and are recorded in profiles/README.md):
-//   ER_OCT_HALF=1          two rows per warp on 16-lane halves (0: one row, 32 lanes)
-//   ER_OCT_MINBLOCKS_F32=5 CTAs/SM for the fp32-class oct kernels (4: 62 regs; 6 spills)
-//   ER_OCT_MINBLOCKS_F64=6 CTAs/SM for the fp64-lerp oct kernel (128 threads each)
-//   ER_OCT_THREADS_F64=128 CTA size of the fp64-lerp oct kernel
+//   ER_OCT_LANES=4         lanes per row, lerp modes (ER_OCT_LANES_NEAREST=8,
+//                          ER_OCT_LANES_F64, ER_OCT_LANES_QUAD=8; the fp32 byte
+//                          path uses 8 when the oct exceeds ER_OCT_BIG_BYTES)
+//   ER_OCT_PAIR=1          fp32 byte path: two voxels per lane per step
+//   ER_CORNER_XU=1         two of the eight corner conversions on the XU pipe
+//   ER_TGT_XU=1            8-bit target values converted on the XU pipe
+//   ER_F64_Q52=1           fp64-lerp mode: Q12.52 coordinates + voxel pairs
+//   ER_REFINE=1            fp64 refinement of ill-conditioned f32 particles
+//   ER_OCT_THREADS=128, ER_OCT_MINBLOCKS_F32=8   fp32-class CTA size / CTAs per SM
+//   ER_OCT_THREADS_F64=128, ER_OCT_MINBLOCKS_F64=6  the same for the fp64-lerp kernel
 //   ER_OCT_SMEM_ACC=1      per-lane fp64 group accumulators in shared memory
-//   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2
+//   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2 (single voxels)
 //   ER_OCT_ACC2=1          px += x; (pxx, pyx) by one FFMA2 of x * (x, y)
 //   ER_BITS_EXACT=1        binary sources: integer counts + fp64 boundary cells
-//                          (0: (px, pxx) by FFMA2 of x * (1, x), 2 more SASS)
 //   ER_FRAC_I2F=1          fractions by I2F on the fixed-point low word
 //   ER_FRAC_RN=1           ... rounded to nearest (0: truncated, biased low)
 //   ER_OCT_TILE_MAJOR=1    tile-major CTA order (0: particle-major)
 //   ER_OCT_UNROLL=1        voxel-loop unroll; ER_OCT_LDPOLICY=0 (.nc; 1 .cg, 2 .cs)
-//   ER_OCT_THREADS=256     CTA size; ER_MIN_TILES=8 minimum tiles per particle
+//   ER_OPAQUE_STEP=0       pair-loop steps held in opaque registers (rejected)
+//   ER_MIN_TILES=8         minimum tiles per particle
 //   ER_BOUNDS_CHECK=0      debug build: every gather index range-checked (common.cuh)
 #include <type_traits>
 
