@@ -119,6 +119,11 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_OCT_LANES_NEAREST
 #define ER_OCT_LANES_NEAREST (ER_OCT_HALF ? 8 : 32)
 #endif
+// perf-only experiments on the pair loop's target loads (see above); never set
+// in a real build
+#ifndef ER_EXP_TGT
+#define ER_EXP_TGT 0
+#endif
 #ifndef ER_OPAQUE_STEP
 #define ER_OPAQUE_STEP 0
 #endif
@@ -949,8 +954,19 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
           const uint2 a8 = ld_oct(oct + (unsigned)er_idx(ca, ncells));
           const uint2 b8 = ld_oct(oct + (unsigned)er_idx(cb, ncells));
           const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
+#if ER_EXP_TGT == 1
+          // perf-only experiment (wrong numbers): voxel b reuses voxel a's
+          // target value -- bounds what sharing a target load between two
+          // samples (e.g. two particles per CTA) could save
+          const TT ya = __ldg(tp);
+          const TT yb = ya;
+#elif ER_EXP_TGT == 2
+          // perf-only experiment (wrong numbers): no target loads at all
+          const TT ya = (TT)(ti & 7), yb = (TT)(ti & 3);
+#else
           const TT ya = __ldg(tp);
           const TT yb = __ldg(tp + kLanes);
+#endif
           const float2 y2 = tgt_add2(ty, ya, yb);
           const float2 fu = __fmul2_rn(make_float2(ER_U2F((unsigned)cu), ER_U2F((unsigned)bu)), sc);
           const float2 fv = __fmul2_rn(make_float2(ER_U2F((unsigned)cv), ER_U2F((unsigned)bv)), sc);
