@@ -1,7 +1,8 @@
 """Multi-rank host logic on CPU (gloo, world_size 2 and 3).
 
 The device path shards particles over ranks with dist.ShardPlan and
-all-gathers the likelihood shards with dist.allgather_shards before the
+all-gathers the likelihood shards (one packed block per rank,
+dist.allgather_packed) before the
 replicated update (smc.DeviceSmcRun.update); the exhaustive search shards
 node ranges and reduces (value, index) pairs with the lowest-index
 tie-break.  Here the same host functions run under torch.distributed/gloo
@@ -184,3 +185,66 @@ def test_score_frames_sharded_over_ranks(world):
         owned += seen[: plan.count]
         assert raised is not None and "frame 6" in raised
     assert sorted(owned) == list(range(7))
+
+
+def _packed_worker(rank, world, port, n, out_q):
+    """One SMC iteration's exchange as DeviceSmcRun does it, on CPU tensors:
+    each rank writes its shard of z and degenerate flags into ONE packed
+    block, ONE all_gather, then every rank reads particle i back the way
+    er_smc_update_gathered's ZPacked accessor does."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = dist.plan(n)
+        S = plan.shard
+        block = dist.packed_block_bytes(S)
+        local = torch.zeros(block, dtype=torch.uint8)
+        z_local = local[: 8 * S].view(torch.float64)
+        dg_local = local[8 * S: 9 * S]
+        g = np.random.default_rng(123)
+        z_all = g.random(n)
+        dg_all = (g.random(n) < 0.2).astype(np.uint8)
+        z_local[: plan.count] = torch.from_numpy(z_all[plan.lo: plan.hi])
+        dg_local[: plan.count] = torch.from_numpy(dg_all[plan.lo: plan.hi])
+        out = torch.zeros(block * world, dtype=torch.uint8)
+        calls = []
+        orig = td.all_gather_into_tensor
+
+        def counting(*a, **k):
+            calls.append(1)
+            return orig(*a, **k)
+
+        td.all_gather_into_tensor = counting
+        try:
+            dist.allgather_packed(local, out)
+        finally:
+            td.all_gather_into_tensor = orig
+        buf = out.numpy()
+        z = np.array([buf[(i // S) * block: (i // S) * block + 8 * S].view(np.float64)[i % S]
+                      for i in range(n)])
+        dg = np.array([buf[(i // S) * block + 8 * S + i % S] for i in range(n)])
+        out_q.put((rank, len(calls), np.array_equal(z, z_all), np.array_equal(dg, dg_all)))
+    finally:
+        td.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 2000), (3, 101), (2, 7)])
+def test_one_packed_allgather_carries_z_and_flags(world, n):
+    """The exchange of an SMC iteration is exactly ONE collective, and the
+    packed rank blocks decode to every particle's z and degenerate flag
+    (the layout er_smc_update_gathered reads; block size % 8 == 0)."""
+    assert dist.packed_block_bytes(n) % 8 == 0 and dist.packed_block_bytes(n) >= 9 * n
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_packed_worker, args=(r, world, port, n, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == list(range(world))
+    for _, ncalls, z_ok, dg_ok in res:
+        assert ncalls == 1 and z_ok and dg_ok
