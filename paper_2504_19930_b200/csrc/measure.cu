@@ -1606,7 +1606,8 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
     char* base = (char*)workspace_dev + partials_bytes(g, P);
     r.count = (int*)base;
     r.list = (int*)(base + 16);
-    if (cudaMemsetAsync(r.count, 0, sizeof(int), st) != cudaSuccess) ER_CHECK_LAUNCH();
+    const cudaError_t e = cudaMemsetAsync(r.count, 0, sizeof(int), st);
+    if (e != cudaSuccess) return er_set_cuda_error(e, "er_measure_ncc (refinement list)");
   }
   measure_finalize_kernel<<<(unsigned)((P + fb - 1) / fb), fb, 0, st>>>(
       part, g.ntiles, P, tgt_moments_dev, nvox, overlap_only ? 1 : 0, f, ncc_dev, degen_dev,
