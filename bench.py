@@ -402,6 +402,12 @@ def run_ours(args):
     l2 = l2_peak_live(dev) if world == 1 else None
     if l2 is not None:
         l2["frac"] = achieved_gbs / l2["peak"]
+        # the kernel's ACTUAL L2->SM read traffic (ncu capture, profiles/
+        # traffic.json) over this run's launch time, against the same peak
+        l2_bytes = (traffic or {}).get("l2_to_sm_read_bytes_per_launch")
+        if l2_bytes:
+            l2["traffic_gbs"] = l2_bytes / (meas_avg * 1e-3) / 1e9
+            l2["traffic_frac"] = l2["traffic_gbs"] / l2["peak"]
     roofline = {
         "bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
         "frac": achieved_gbs / peak,
