@@ -140,6 +140,10 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_OCT_PAIR
 #define ER_OCT_PAIR 1
 #endif
+// bit-oct (binary) path: two voxels per lane per step
+#ifndef ER_OCT_PAIR_BITS
+#define ER_OCT_PAIR_BITS 1
+#endif
 #ifndef ER_OCT_UNROLL
 #define ER_OCT_UNROLL 1
 #endif
@@ -701,6 +705,31 @@ __device__ __forceinline__ double lerp_q52(uint2 c8, long long cu, long long cv,
   return fma(fw, c1 - c0, c0) - 4503599627370496.0;
 }
 
+// Bit-oct boundary cell (corner bits neither all 0 nor all 1): the trilinear
+// sample in fp64 from the exact 32-bit fractions of Q32.32 coordinates, added
+// to the lane's fp64 accumulators in shared memory.  The u-lerp of two 0/1
+// corners is 0, fu, 1 - fu (exact for a 32-bit fraction) or 1 -- the values
+// fma(fu, b1 - b0, b0) takes -- so it is done by selects.
+__device__ __forceinline__ void bits_boundary(unsigned c, long long cu, long long cv,
+                                              long long cw, double y, double3& acc) {
+  using F = Fix<32>;
+  const double fu = F::frac64(cu), fv = F::frac64(cv), fw = F::frac64(cw);
+  const double gu = 1.0 - fu;
+  auto pair = [c, fu, gu](int b) {
+    const unsigned lo = (c >> b) & 1u, hi = (c >> (b + 1)) & 1u;
+    return lo ? (hi ? 1.0 : gu) : (hi ? fu : 0.0);
+  };
+  const double c00 = pair(0), c10 = pair(2), c01 = pair(4), c11 = pair(6);
+  const double c0 = fma(fv, c10 - c00, c00);
+  const double c1 = fma(fv, c11 - c01, c01);
+  const double x = fma(fw, c1 - c0, c0);
+  double3 a = acc;
+  a.x += x;
+  a.y = fma(x, x, a.y);
+  a.z = fma(y, x, a.z);
+  acc = a;
+}
+
 struct RowRec {  // one target row of a 32-row group, in fixed point
   long long fu0, fv0, fw0;
   int klo, khi, off, pad;
@@ -816,6 +845,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   const int sub = lane & (kLanes - 1);
   // fp32 byte path: voxels k and k + kLanes of a lane are sampled together
   constexpr bool kPair = ER_OCT_PAIR && LERP == ER_LERP_F32 && !BITS;
+  constexpr bool kPairBits = ER_OCT_PAIR_BITS && ER_BITS_EXACT && LERP == ER_LERP_F32 && kBits;
   const long long du1 = kLanes * du, dv1 = kLanes * dv, dw1 = kLanes * dw;
   long long du2 = 2 * du1, dv2 = 2 * dv1, dw2 = 2 * dw1;
 #if ER_OPAQUE_STEP
@@ -930,6 +960,48 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
           qyx = fma(ya, xa, qyx);
         }
         k = qhi;
+      }
+      if (kPairBits) {
+        // binary source, two voxels per lane per step (k and k + kLanes): two
+        // independent byte gathers in flight per lane, shared loop test and
+        // target address; uniform cells add integer counts, boundary cells
+        // interpolate in fp64 (bits_boundary)
+        int ti = toff + k;
+        const int ti_end = toff + qhi - kLanes;
+        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
+        const uint8_t* __restrict__ bytes = reinterpret_cast<const uint8_t*>(oct);
+        for (; ti < ti_end; ti += 2 * kLanes) {
+          const int ca = (F::ipart(cu) * og.cy + F::ipart(cv)) * og.cz + F::ipart(cw);
+          const int cb = (F::ipart(bu) * og.cy + F::ipart(bv)) * og.cz + F::ipart(bw);
+          const unsigned c_a = __ldg(bytes + (unsigned)er_idx(ca, ncells));
+          const unsigned c_b = __ldg(bytes + (unsigned)er_idx(cb, ncells));
+          const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
+          const TT ya = __ldg(tp);
+          const TT yb = __ldg(tp + kLanes);
+          const auto yfa = ty.add(ya);
+          const auto yfb = ty.add(yb);
+          if (c_a == 0xFFu) {
+            ++ones;
+            if (kU8Tgt) ones_y += (unsigned)ya;
+            else pyx += (float)yfa;
+          } else if (c_a != 0u) {
+            bits_boundary(c_a, cu, cv, cw, (double)yfa, racc[threadIdx.x]);
+          }
+          if (c_b == 0xFFu) {
+            ++ones;
+            if (kU8Tgt) ones_y += (unsigned)yb;
+            else pyx += (float)yfb;
+          } else if (c_b != 0u) {
+            bits_boundary(c_b, bu, bv, bw, (double)yfb, racc[threadIdx.x]);
+          }
+          cu += du2;
+          cv += dv2;
+          cw += dw2;
+          bu += du2;
+          bv += dv2;
+          bw += dw2;
+        }
+        k = ti - toff;
       }
       if (kPair) {
         // two voxels per lane per step (k and k + kLanes): the fractions, the
