@@ -144,6 +144,10 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_OCT_PAIR_BITS
 #define ER_OCT_PAIR_BITS 1
 #endif
+// quad (f32/f64 source) path: two voxels per lane per step
+#ifndef ER_OCT_PAIR_QUAD
+#define ER_OCT_PAIR_QUAD 1
+#endif
 #ifndef ER_OCT_UNROLL
 #define ER_OCT_UNROLL 1
 #endif
@@ -705,6 +709,18 @@ __device__ __forceinline__ double lerp_q52(uint2 c8, long long cu, long long cv,
   return fma(fw, c1 - c0, c0) - 4503599627370496.0;
 }
 
+// fp32 trilinear sample from two quad entries (planes k0, k1), each
+// (x[i0][j0], x[i0][j1], x[i1][j0], x[i1][j1]): u-lerps packed over j.
+__device__ __forceinline__ float lerp_quad(float4 q0, float4 q1, float fu, float fv, float fw) {
+  const float2 fu2 = make_float2(fu, fu);
+  const float2 a0 = make_float2(q0.x, q0.y), a1 = make_float2(q1.x, q1.y);
+  const float2 p0 = __ffma2_rn(fu2, f2sub(make_float2(q0.z, q0.w), a0), a0);  // (c00, c10)
+  const float2 p1 = __ffma2_rn(fu2, f2sub(make_float2(q1.z, q1.w), a1), a1);  // (c01, c11)
+  const float c0 = fmaf(fv, p0.y - p0.x, p0.x);
+  const float c1 = fmaf(fv, p1.y - p1.x, p1.x);
+  return fmaf(fw, c1 - c0, c0);
+}
+
 // Bit-oct boundary cell (corner bits neither all 0 nor all 1): the trilinear
 // sample in fp64 from the exact 32-bit fractions of Q32.32 coordinates, added
 // to the lane's fp64 accumulators in shared memory.  The u-lerp of two 0/1
@@ -846,6 +862,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   // fp32 byte path: voxels k and k + kLanes of a lane are sampled together
   constexpr bool kPair = ER_OCT_PAIR && LERP == ER_LERP_F32 && !BITS;
   constexpr bool kPairBits = ER_OCT_PAIR_BITS && ER_BITS_EXACT && LERP == ER_LERP_F32 && kBits;
+  constexpr bool kPairQuad = ER_OCT_PAIR_QUAD && kQuad;
   const long long du1 = kLanes * du, dv1 = kLanes * dv, dw1 = kLanes * dw;
   long long du2 = 2 * du1, dv2 = 2 * dv1, dw2 = 2 * dw1;
 #if ER_OPAQUE_STEP
@@ -961,6 +978,39 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
         }
         k = qhi;
       }
+      if (kPairQuad) {
+        // quad layout, two voxels per lane per step (k and k + kLanes): four
+        // 16-byte gathers in flight per lane, shared loop test and target
+        // address; per voxel exactly the single-voxel arithmetic
+        int ti = toff + k;
+        const int ti_end = toff + qhi - kLanes;
+        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
+        const float4* __restrict__ qd = reinterpret_cast<const float4*>(oct);
+        const float s32 = 2.3283064365386963e-10f;  // 2^-32
+        for (; ti < ti_end; ti += 2 * kLanes) {
+          const int ca = (F::ipart(cu) * og.cy + F::ipart(cv)) * og.cz + F::ipart(cw);
+          const int cb = (F::ipart(bu) * og.cy + F::ipart(bv)) * og.cz + F::ipart(bw);
+          const float4* qa = qd + (unsigned)er_idx(ca, ncells - 1);
+          const float4* qb = qd + (unsigned)er_idx(cb, ncells - 1);
+          const float4 a0 = __ldg(qa), a1 = __ldg(qa + 1), b0 = __ldg(qb), b1 = __ldg(qb + 1);
+          const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
+          const float ya = (float)ty.add(__ldg(tp));
+          const float yb = (float)ty.add(__ldg(tp + kLanes));
+          const float2 sc = make_float2(s32, s32);
+          const float2 fu = __fmul2_rn(make_float2(ER_U2F((unsigned)cu), ER_U2F((unsigned)bu)), sc);
+          const float2 fv = __fmul2_rn(make_float2(ER_U2F((unsigned)cv), ER_U2F((unsigned)bv)), sc);
+          const float2 fw = __fmul2_rn(make_float2(ER_U2F((unsigned)cw), ER_U2F((unsigned)bw)), sc);
+          acc_voxel(lerp_quad(a0, a1, fu.x, fv.x, fw.x), ya, px, pxx, pyx);
+          acc_voxel(lerp_quad(b0, b1, fu.y, fv.y, fw.y), yb, px, pxx, pyx);
+          cu += du2;
+          cv += dv2;
+          cw += dw2;
+          bu += du2;
+          bv += dv2;
+          bw += dw2;
+        }
+        k = ti - toff;
+      }
       if (kPairBits) {
         // binary source, two voxels per lane per step (k and k + kLanes): two
         // independent byte gathers in flight per lane, shared loop test and
@@ -1075,14 +1125,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
                                         make_float2(2.3283064365386963e-10f,
                                                     2.3283064365386963e-10f));
           const float fw = F::frac32(cw);
-          const float2 fu2 = make_float2(fuv.x, fuv.x);
-          // u-lerps packed over j: (c00, c10) on plane k0, (c01, c11) on k1
-          const float2 a0 = make_float2(q0.x, q0.y), a1 = make_float2(q1.x, q1.y);
-          const float2 p0 = __ffma2_rn(fu2, f2sub(make_float2(q0.z, q0.w), a0), a0);
-          const float2 p1 = __ffma2_rn(fu2, f2sub(make_float2(q1.z, q1.w), a1), a1);
-          const float c0 = fmaf(fuv.y, p0.y - p0.x, p0.x);
-          const float c1 = fmaf(fuv.y, p1.y - p1.x, p1.x);
-          acc_voxel(fmaf(fw, c1 - c0, c0), (float)yv, px, pxx, pyx);
+          acc_voxel(lerp_quad(q0, q1, fuv.x, fuv.y, fw), (float)yv, px, pxx, pyx);
           cu += du1;
           cv += dv1;
           cw += dw1;
