@@ -144,6 +144,17 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_OCT_PAIR_BITS
 #define ER_OCT_PAIR_BITS 1
 #endif
+// voxels per lane per step of the bit-oct loop: 2 at 4 lanes per row; 4 at
+// the 8 lanes per row used for long target rows (nz >= ER_BITS_WIDE_NZ)
+#ifndef ER_BITS_NB
+#define ER_BITS_NB 2
+#endif
+#ifndef ER_BITS_NB_WIDE
+#define ER_BITS_NB_WIDE 4
+#endif
+#ifndef ER_BITS_WIDE_NZ
+#define ER_BITS_WIDE_NZ 128
+#endif
 // quad (f32/f64 source) path: two voxels per lane per step
 #ifndef ER_OCT_PAIR_QUAD
 #define ER_OCT_PAIR_QUAD 1
@@ -1012,46 +1023,52 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
         k = ti - toff;
       }
       if (kPairBits) {
-        // binary source, two voxels per lane per step (k and k + kLanes): two
+        // binary source, NB voxels per lane per step (k, k + kLanes, ...): NB
         // independent byte gathers in flight per lane, shared loop test and
         // target address; uniform cells add integer counts, boundary cells
-        // interpolate in fp64 (bits_boundary)
+        // interpolate in fp64 (bits_boundary).  Voxels are visited in the
+        // single-voxel loop's order, so the results are bit-identical to it.
+        constexpr int NB = kLanes >= 8 ? ER_BITS_NB_WIDE : ER_BITS_NB;
         int ti = toff + k;
-        const int ti_end = toff + qhi - kLanes;
-        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
+        const int ti_end = toff + qhi - (NB - 1) * kLanes;
+        long long qu[NB], qv[NB], qw[NB];
+#pragma unroll
+        for (int m = 0; m < NB; ++m) {
+          qu[m] = cu + m * du1;
+          qv[m] = cv + m * dv1;
+          qw[m] = cw + m * dw1;
+        }
+        const long long duN = NB * du1, dvN = NB * dv1, dwN = NB * dw1;
         const uint8_t* __restrict__ bytes = reinterpret_cast<const uint8_t*>(oct);
-        for (; ti < ti_end; ti += 2 * kLanes) {
-          const int ca = (F::ipart(cu) * og.cy + F::ipart(cv)) * og.cz + F::ipart(cw);
-          const int cb = (F::ipart(bu) * og.cy + F::ipart(bv)) * og.cz + F::ipart(bw);
-          const unsigned c_a = __ldg(bytes + (unsigned)er_idx(ca, ncells));
-          const unsigned c_b = __ldg(bytes + (unsigned)er_idx(cb, ncells));
+        for (; ti < ti_end; ti += NB * kLanes) {
+          unsigned cc[NB];
+          TT yy[NB];
           const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
-          const TT ya = __ldg(tp);
-          const TT yb = __ldg(tp + kLanes);
-          const auto yfa = ty.add(ya);
-          const auto yfb = ty.add(yb);
-          if (c_a == 0xFFu) {
-            ++ones;
-            if (kU8Tgt) ones_y += (unsigned)ya;
-            else pyx += (float)yfa;
-          } else if (c_a != 0u) {
-            bits_boundary(c_a, cu, cv, cw, (double)yfa, racc[threadIdx.x]);
+#pragma unroll
+          for (int m = 0; m < NB; ++m) {
+            const int cm = (F::ipart(qu[m]) * og.cy + F::ipart(qv[m])) * og.cz + F::ipart(qw[m]);
+            cc[m] = __ldg(bytes + (unsigned)er_idx(cm, ncells));
+            yy[m] = __ldg(tp + m * kLanes);
           }
-          if (c_b == 0xFFu) {
-            ++ones;
-            if (kU8Tgt) ones_y += (unsigned)yb;
-            else pyx += (float)yfb;
-          } else if (c_b != 0u) {
-            bits_boundary(c_b, bu, bv, bw, (double)yfb, racc[threadIdx.x]);
+#pragma unroll
+          for (int m = 0; m < NB; ++m) {
+            const auto yf = ty.add(yy[m]);
+            if (cc[m] == 0xFFu) {
+              ++ones;
+              if (kU8Tgt) ones_y += (unsigned)yy[m];
+              else pyx += (float)yf;
+            } else if (cc[m] != 0u) {
+              bits_boundary(cc[m], qu[m], qv[m], qw[m], (double)yf, racc[threadIdx.x]);
+            }
+            qu[m] += duN;
+            qv[m] += dvN;
+            qw[m] += dwN;
           }
-          cu += du2;
-          cv += dv2;
-          cw += dw2;
-          bu += du2;
-          bv += dv2;
-          bw += dw2;
         }
         k = ti - toff;
+        cu = qu[0];
+        cv = qv[0];
+        cw = qw[0];
       }
       if (kPair) {
         // two voxels per lane per step (k and k + kLanes): the fractions, the
@@ -1658,11 +1675,26 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
       measure_oct_kernel<TT, L, B, 0><<<blocks, OctThreads<L>::n, 0, st>>>(                \
           (const TT*)tgt->data_dev, lay, A_dev, b_dev, g, og, part);                       \
   } while (0)
+#define ER_OCT_BITS_WIDE(TT)                                                               \
+  do {                                                                                     \
+    if (overlap_only)                                                                      \
+      measure_oct_kernel<TT, ER_LERP_F32, 1, 1, 8>                                         \
+          <<<blocks, OctThreads<ER_LERP_F32>::n, 0, st>>>((const TT*)tgt->data_dev, lay,   \
+                                                          A_dev, b_dev, g, og, part);      \
+    else                                                                                   \
+      measure_oct_kernel<TT, ER_LERP_F32, 1, 0, 8>                                         \
+          <<<blocks, OctThreads<ER_LERP_F32>::n, 0, st>>>((const TT*)tgt->data_dev, lay,   \
+                                                          A_dev, b_dev, g, og, part);      \
+  } while (0)
 #define ER_OCT_BITS(TT)                                                   \
   do {                                                                    \
     if (lerp_mode == ER_LERP_NEAREST) ER_OCT(TT, ER_LERP_NEAREST, 1);     \
+    else if (wide_rows) ER_OCT_BITS_WIDE(TT);                             \
     else ER_OCT(TT, ER_LERP_F32, 1);                                      \
   } while (0)
+    // long target rows: the mask path walks them with 8 lanes, 4 voxels each
+    // per step (more gathers in flight per lane)
+    const bool wide_rows = tgt->nz >= ER_BITS_WIDE_NZ;
 #define ER_OCT_BIG(TT)                                                                     \
   do {                                                                                     \
     if (overlap_only)                                                                      \
@@ -1696,6 +1728,7 @@ extern "C" int er_measure_ncc(const er_volume* tgt, const er_volume* src,
       }
     }
 #undef ER_OCT_BITS
+#undef ER_OCT_BITS_WIDE
 #undef ER_OCT_BYTES
 #undef ER_OCT_BIG
 #undef ER_OCT
