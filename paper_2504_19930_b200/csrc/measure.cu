@@ -872,7 +872,8 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
   const int sub = lane & (kLanes - 1);
   // fp32 byte path: voxels k and k + kLanes of a lane are sampled together
   constexpr bool kPair = ER_OCT_PAIR && LERP == ER_LERP_F32 && !BITS;
-  constexpr bool kPairBits = ER_OCT_PAIR_BITS && ER_BITS_EXACT && LERP == ER_LERP_F32 && kBits;
+  constexpr bool kPairBits = ER_OCT_PAIR_BITS && ER_BITS_EXACT && kBits &&
+                             (LERP == ER_LERP_F32 || LERP == ER_LERP_NEAREST);
   constexpr bool kPairQuad = ER_OCT_PAIR_QUAD && kQuad;
   const long long du1 = kLanes * du, dv1 = kLanes * dv, dw1 = kLanes * dw;
   long long du2 = 2 * du1, dv2 = 2 * dv1, dw2 = 2 * dw1;
@@ -1053,7 +1054,16 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
 #pragma unroll
           for (int m = 0; m < NB; ++m) {
             const auto yf = ty.add(yy[m]);
-            if (cc[m] == 0xFFu) {
+            if (LERP == ER_LERP_NEAREST) {
+              // corner bit: fraction >= 0.5 <=> bit 31 of the fixed-point word
+              const unsigned bsel = ((unsigned)qu[m] >> 31) | (((unsigned)qv[m] >> 31) << 1) |
+                                    (((unsigned)qw[m] >> 31) << 2);
+              if ((cc[m] >> bsel) & 1u) {
+                ++ones;
+                if (kU8Tgt) ones_y += (unsigned)yy[m];
+                else pyx += (float)yf;
+              }
+            } else if (cc[m] == 0xFFu) {
               ++ones;
               if (kU8Tgt) ones_y += (unsigned)yy[m];
               else pyx += (float)yf;
