@@ -68,3 +68,46 @@ def test_pipeline_scores_on_an_echo_cycle_match_the_reference_algorithms():
         mm = (ok.resample_trilinear(sm, am, bm, tf.dims, ok.max_threads()) > 0.5)
         assert rep.dsc_before[f] == pc.dice_ref(tm, sm)
         assert rep.dsc_after[f] == pc.dice_ref(mm.astype(np.float64), tm)
+
+
+def test_c5_scale_measurement_matches_the_oracle_and_is_batch_invariant():
+    """BASELINE configs[4] at full size: the 256^3 z-scored echo pair (its oct
+    layout, 136 MB, exceeds L2, so the kernel runs the 8-lanes-per-row
+    variant), 16,384 particles of SMC iteration 0 measured in one launch.
+    Per-particle parity on a spread of 48 of them against the bit-exact C
+    oracle (f32 bar 1e-4, counts exact) and two size-independent properties
+    of the full batch: every particle's result is bitwise the same when it is
+    measured alone in a small batch (fixed tiling: batch/shard invariance),
+    and z is in [0, 1]."""
+    sys.path.insert(0, ROOT)
+    import torch
+
+    from oracle import kernels as ok
+    from paper_2504_19930_b200 import Executor, SmcConfig, normalize_zscore, ops
+    from paper_2504_19930_b200 import smc as dsmc
+    from paper_2504_19930_b200.phantom_device import echo_case_device
+
+    case = echo_case_device(dims=(256, 256, 256), spacing=(0.8, 0.8, 0.8), frames=1, seed=0)
+    t = normalize_zscore(case.target.frames[0])
+    s = normalize_zscore(case.source.frames[0])
+    P = 16384
+    run = dsmc.DeviceSmcRun(t, s, SmcConfig(mode="image", n_particles=P, n_iterations=1, seed=0),
+                            Executor())
+    run.predict(0)
+    run.measure()
+    z = run.z_local[:P].cpu().numpy().copy()
+    n = run.n_local[:P].cpu().numpy().copy()
+    dg = run.dg_local[:P].cpu().numpy().astype(bool)
+    assert np.all((z >= 0) & (z <= 1))
+    idx = np.linspace(0, P - 1, 48).astype(np.int64)
+    A = run.A[:P][torch.as_tensor(idx, device=run.A.device)].contiguous()
+    B = run.B[:P][torch.as_tensor(idx, device=run.B.device)].contiguous()
+    zs, ds, ns = (x.cpu().numpy() for x in ops.measure(run.tdv, run.sdv, A, B, False, "f32"))
+    assert np.array_equal(zs, z[idx]) and np.array_equal(ns, n[idx])
+    assert np.array_equal(ds.astype(bool), dg[idx])
+    a = A.cpu().numpy().reshape(-1, 3, 3)
+    b = B.cpu().numpy()
+    zo, do, no = ok.ncc_measure_batch(t.data, s.data, a, b, False, ok.max_threads(),
+                                      return_counts=True)
+    assert np.array_equal(ns, no) and np.array_equal(ds.astype(bool), do)
+    assert np.all(np.abs(zs - zo) <= 1e-4 * np.abs(zo) + 1e-12)
