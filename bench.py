@@ -416,13 +416,17 @@ def run_ours(args):
         "note": ("achieved = sampled (in-bounds) voxels x 9 algorithmic bytes (8 oct "
                  "corner bytes + 1 target byte) / measurement time: an HBM-equivalent "
                  "rate.  Both volumes are L2-resident, so the DRAM traffic per launch "
-                 "(`traffic`, ncu) is only the compulsory volume reads; `l2` is the same "
-                 "rate against the L2 read bandwidth measured live in this run."),
+                 "(`traffic`, ncu; `dram_gbs` per launch time) is only the compulsory "
+                 "volume reads; `l2` is the same rate against the L2 read bandwidth "
+                 "measured live in this run, plus the kernel's actual L2->SM traffic."),
         "l2": l2,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
         "bytes_per_sampled_voxel": bytes_per_unit,
         "sampled_voxels_per_launch": sampled,
         "kernel_ms": meas_avg,
+        # measured DRAM traffic (ncu) per launch time: the HBM the kernel
+        # actually uses -- the compulsory volume reads only
+        "dram_gbs": ((traffic or {}).get("dram_bytes_per_launch") or 0) / (meas_avg * 1e-3) / 1e9,
         "sampled_voxels_per_s": sampled / (meas_avg * 1e-3),
         "kernel_share_of_step": meas_avg / ms_per_step,
         "pre_ms_per_step": sum(pre_ms) / len(pre_ms),
