@@ -136,3 +136,43 @@ def test_c3_full_4d_pipeline_matches_reference():
     assert got["aggregates"].keys() == want["aggregates"].keys()
     for k, v in want["aggregates"].items():
         assert got["aggregates"][k] == pytest.approx(v, rel=1e-6, abs=1e-9), k
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_c2_overlap_region_registration_matches_reference(c2, precision):
+    """The C2 pair with SmcConfig(ncc_region="overlap"), 2000 x 20, seed 3:
+    the overlap-region kernels (in-bounds target sums and sums of squares,
+    /root/reference/pkg/src/echoreg/kernels_numba.py:172-189) against the real
+    reference's run (tests/golden/full_c2o.npz)."""
+    from paper_2504_19930_b200 import Executor, SmcConfig
+    from paper_2504_19930_b200 import smc as dsmc
+
+    path = os.path.join(GOLDEN, "full_c2o.npz")
+    if not os.path.exists(path):
+        pytest.skip("full_c2o.npz not generated")
+    g = np.load(path)
+    _, t, s = c2
+    assert str(g["c2o_target_sha256"]) == str(c2[0]["c2_target_sha256"])
+    cfg = SmcConfig(mode="image", n_particles=2000, n_iterations=20, seed=3,
+                    ncc_region="overlap")
+    run = dsmc.DeviceSmcRun(t, s, cfg, Executor(precision=precision))
+    z = {}
+    for k in range(cfg.n_iterations):
+        run.predict(k)
+        run.measure()
+        if k in (0, cfg.n_iterations - 1):
+            z[k] = (run.z_local[:2000].cpu().numpy().copy(),
+                    run.dg_local[:2000].cpu().numpy().astype(bool))
+        run.update(k)
+    tr = run.finish()
+    rot, vox = _transform_diff(tr.estimates[-1].to_array(), g["c2o_estimate"], t.spacing)
+    assert rot <= 0.1 and vox <= 0.1, (rot, vox)
+    assert np.array_equal(np.array(tr.resampled), g["c2o_resampled"])
+    ess = np.array(tr.ess)
+    assert np.max(np.abs(ess - g["c2o_ess"]) / g["c2o_ess"]) <= ESS_RTOL[precision]
+    for k, key in ((0, "first"), (cfg.n_iterations - 1, "last")):
+        zz, dd = z[k]
+        zr, dr = g[f"c2o_z_{key}"], g[f"c2o_degen_{key}"]
+        assert np.array_equal(dd, dr), key
+        rel = np.abs(zz - zr) / np.maximum(np.abs(zr), 1e-300)
+        assert rel.max() <= Z_RTOL[precision], (key, float(rel.max()))
