@@ -137,6 +137,11 @@ constexpr int kRowsPerTile = 2048;
 #endif
 
 // fp32 byte path: two voxels per lane per step, lerps packed across them
+// fp32 byte pair loop: step fraction words + one cell index per voxel
+// instead of 64-bit fixed-point coordinates
+#ifndef ER_PAIR_CELLSTEP
+#define ER_PAIR_CELLSTEP 1
+#endif
 #ifndef ER_OCT_PAIR
 #define ER_OCT_PAIR 1
 #endif
@@ -533,6 +538,32 @@ __device__ __forceinline__ double byte_m64(unsigned w, unsigned sel) {
   return __hiloint2double(0x43300000, __byte_perm(w, 0u, sel | 0x4440u));
 }
 
+
+// One step of the cell-index coordinates (ER_PAIR_CELLSTEP): fraction words
+// (u, v, w) + (lu, lv, lw) with the carries as explicit PTX carry chains; the
+// cell index moves by h (the step's integer parts times the strides) plus
+// cyz / cz / 1 for each carried axis.
+__device__ __forceinline__ int cell_step(unsigned u, unsigned v, unsigned w, int cell, unsigned lu,
+                                         unsigned lv, unsigned lw, int h, int cyz, int cz,
+                                         unsigned& ou, unsigned& ov, unsigned& ow) {
+  int out;
+  asm("{\n\t.reg .u32 fu, fv;\n\t.reg .pred pu, pv;\n\t"
+      "add.cc.u32 %0, %4, %8;\n\t"
+      "addc.u32 fu, 0, 0;\n\t"
+      "add.cc.u32 %1, %5, %9;\n\t"
+      "addc.u32 fv, 0, 0;\n\t"
+      "add.cc.u32 %2, %6, %10;\n\t"
+      "addc.u32 %3, %7, %11;\n\t"
+      "setp.ne.u32 pu, fu, 0;\n\t"
+      "setp.ne.u32 pv, fv, 0;\n\t"
+      "selp.u32 fu, %12, 0, pu;\n\t"
+      "selp.u32 fv, %13, 0, pv;\n\t"
+      "add.u32 %3, %3, fu;\n\t"
+      "add.u32 %3, %3, fv;\n\t}"
+      : "=r"(ou), "=r"(ov), "=r"(ow), "=r"(out)
+      : "r"(u), "r"(v), "r"(w), "r"(cell), "r"(lu), "r"(lv), "r"(lw), "r"(h), "r"(cyz), "r"(cz));
+  return out;
+}
 
 // Fixed-point source coordinates with FB fractional bits.  FB = 32 (fp32
 // lerps): the integer part is the high register, the fraction the low one.
@@ -996,9 +1027,9 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
         // address; per voxel exactly the single-voxel arithmetic
         int ti = toff + k;
         const int ti_end = toff + qhi - kLanes;
-        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
         const float4* __restrict__ qd = reinterpret_cast<const float4*>(oct);
         const float s32 = 2.3283064365386963e-10f;  // 2^-32
+        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
         for (; ti < ti_end; ti += 2 * kLanes) {
           const int ca = (F::ipart(cu) * og.cy + F::ipart(cv)) * og.cz + F::ipart(cw);
           const int cb = (F::ipart(bu) * og.cy + F::ipart(bv)) * og.cz + F::ipart(bw);
@@ -1092,6 +1123,46 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
         // loop test and the target address
         int ti = toff + k;
         const int ti_end = toff + qhi - kLanes;
+#if ER_PAIR_CELLSTEP
+        // cell-index stepping: the fixed-point coordinates live as their
+        // 32-bit fraction words plus ONE padded cell index per voxel; a step
+        // adds the fraction words (the carries are the integer parts'
+        // +1s) and moves the cell index by the steps' integer parts times
+        // the strides (h1 / h2) plus the strides of the carried axes.  Voxel
+        // b = voxel a + kLanes is derived from a every step.
+        unsigned au = (unsigned)cu, av = (unsigned)cv, aw = (unsigned)cw;
+        int cella = (F::ipart(cu) * og.cy + F::ipart(cv)) * og.cz + F::ipart(cw);
+        const unsigned l1u = (unsigned)du1, l1v = (unsigned)dv1, l1w = (unsigned)dw1;
+        const unsigned l2u = (unsigned)du2, l2v = (unsigned)dv2, l2w = (unsigned)dw2;
+        const int h1 = F::ipart(du1) * cyz + F::ipart(dv1) * og.cz + F::ipart(dw1);
+        const int h2 = F::ipart(du2) * cyz + F::ipart(dv2) * og.cz + F::ipart(dw2);
+        const int ti0 = ti;
+        for (; ti < ti_end; ti += 2 * kLanes) {
+          unsigned bu, bv, bw;
+          const int cellb = cell_step(au, av, aw, cella, l1u, l1v, l1w, h1, cyz, og.cz, bu, bv, bw);
+          const uint2 a8 = ld_oct(oct + (unsigned)er_idx(cella, ncells));
+          const uint2 b8 = ld_oct(oct + (unsigned)er_idx(cellb, ncells));
+          const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
+          const TT ya = __ldg(tp);
+          const TT yb = __ldg(tp + kLanes);
+          const float2 y2 = tgt_add2(ty, ya, yb);
+          const float2 fu = __fmul2_rn(make_float2(ER_U2F(au), ER_U2F(bu)), sc);
+          const float2 fv = __fmul2_rn(make_float2(ER_U2F(av), ER_U2F(bv)), sc);
+          const float2 fw = __fmul2_rn(make_float2(ER_U2F(aw), ER_U2F(bw)), sc);
+          const float2 x = lerp_oct_f32x2(a8, b8, fu, fv, fw);
+          sx2 = __fadd2_rn(sx2, x);
+          sxx2 = __ffma2_rn(x, x, sxx2);
+          syx2 = __ffma2_rn(x, y2, syx2);
+          cella = cell_step(au, av, aw, cella, l2u, l2v, l2w, h2, cyz, og.cz, au, av, aw);
+        }
+        {
+          // the 64-bit coordinates for the single-voxel tail
+          const long long np = (ti - ti0) / (2 * kLanes);
+          cu += np * du2;
+          cv += np * dv2;
+          cw += np * dw2;
+        }
+#else
         // voxel b = voxel a + kLanes along the row: its own coordinate set,
         // both stepped by 2 kLanes per iteration
         long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
@@ -1131,6 +1202,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n,
           bv += dv2;
           bw += dw2;
         }
+#endif
         k = ti - toff;
         px = sx2.x + sx2.y;
         pxx = sxx2.x + sxx2.y;

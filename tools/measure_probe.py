@@ -40,3 +40,7 @@ for prec in precs:
                      sampled_per_s=nin / (ms * 1e-3), inbounds_frac=nin / (P * nvox),
                      hbm_frac_9B=nin * 9 / (ms * 1e-3) / 6535.4e9)
     print(prec, json.dumps(res[prec]), flush=True)
+    if os.environ.get("ER_PROBE_DUMP"):
+        # raw outputs, to compare builds bit for bit
+        torch.save({"z": z.cpu(), "d": d.cpu(), "n": n.cpu()},
+                   f"{os.environ['ER_PROBE_DUMP']}_{prec}.pt")
