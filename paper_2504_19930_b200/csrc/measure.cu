@@ -41,6 +41,8 @@
 //   ER_F64_Q52=1           fp64-lerp mode: Q12.52 coordinates + voxel pairs
 //   ER_REFINE=1            fp64 refinement of ill-conditioned f32 particles
 //   ER_OCT_THREADS=128, ER_OCT_MINBLOCKS_F32=8   fp32-class CTA size / CTAs per SM
+//   ER_OCT_MINBLOCKS_NEAREST=10 (_BITS, _QUAD = 8)  per-path CTAs per SM
+//   ER_PAIR_CELLSTEP=1     byte pair loop: fraction words + one cell index per voxel
 //   ER_OCT_THREADS_F64=128, ER_OCT_MINBLOCKS_F64=6  the same for the fp64-lerp kernel
 //   ER_OCT_SMEM_ACC=1      per-lane fp64 group accumulators in shared memory
 //   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2 (single voxels)
@@ -195,6 +197,18 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 #endif
 #ifndef ER_OCT_MINBLOCKS_F64
 #define ER_OCT_MINBLOCKS_F64 (3 * 256 / ER_OCT_THREADS_F64)
+#endif
+// per-path CTAs per SM: nearest-neighbour byte sampling 10 (14.6 vs 16.3 ms
+// on C2 at 8: fewer registers, more warps to hide the gathers); the bit-oct
+// mask path and the quad layout keep 8 (10 / 12 measured ±0 / slower)
+#ifndef ER_OCT_MINBLOCKS_NEAREST
+#define ER_OCT_MINBLOCKS_NEAREST 10
+#endif
+#ifndef ER_OCT_MINBLOCKS_BITS
+#define ER_OCT_MINBLOCKS_BITS ER_OCT_MINBLOCKS_F32
+#endif
+#ifndef ER_OCT_MINBLOCKS_QUAD
+#define ER_OCT_MINBLOCKS_QUAD ER_OCT_MINBLOCKS_F32
 #endif
 #ifndef ER_MIN_TILES
 #define ER_MIN_TILES 8
@@ -816,9 +830,17 @@ struct OctLanes {
                                                      : ER_OCT_LANES;
 };
 
+template <int LERP, int BITS>
+struct OctMinBlocks {
+  static constexpr int n = LERP == ER_LERP_F64 ? ER_OCT_MINBLOCKS_F64
+                           : BITS == 1         ? ER_OCT_MINBLOCKS_BITS
+                           : BITS == 2         ? ER_OCT_MINBLOCKS_QUAD
+                           : LERP == ER_LERP_NEAREST ? ER_OCT_MINBLOCKS_NEAREST
+                                                     : ER_OCT_MINBLOCKS_F32;
+};
+
 template <typename TT, int LERP, int BITS, int OVL, int LN = 0>
-__global__ void __launch_bounds__(OctThreads<LERP>::n,
-                                   LERP != ER_LERP_F64 ? ER_OCT_MINBLOCKS_F32 : ER_OCT_MINBLOCKS_F64)
+__global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>::n)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
                        const OctGeom og, Partial* __restrict__ part) {

@@ -1,5 +1,6 @@
 """Dev probe: measurement-kernel throughput on the C2 workload (CUDA events
-on the launching stream).  usage: measure_probe.py [P] [precisions] [reps]"""
+on the launching stream).  usage: measure_probe.py [P] [precisions] [reps]
+(ER_PROBE_MODE=mask: the binary masks of the same pair)"""
 import json
 import os
 import sys
@@ -17,8 +18,13 @@ import bench  # noqa: E402
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
 precs = sys.argv[2].split(",") if len(sys.argv) > 2 else ["f32", "f64", "exact"]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
-t, s, _ = bench.make_workload()
-cfg = SmcConfig(mode="image", n_particles=P, n_iterations=1, seed=0)
+t, s, case = bench.make_workload()
+mode = os.environ.get("ER_PROBE_MODE", "image")
+if mode == "mask":
+    # the C3-style binary masks of the same pair (bit-oct path)
+    from paper_2504_19930_b200 import binarize  # noqa: E402
+    t, s = binarize(case.target_masks[0], 0.5), binarize(case.source_masks[0], 0.5)
+cfg = SmcConfig(mode=mode, n_particles=P, n_iterations=1, seed=0)
 run = dsmc.DeviceSmcRun(t, s, cfg, Executor())
 run.predict(0)
 A, B = run.A[:P], run.B[:P]
