@@ -141,6 +141,9 @@ constexpr int kRowsPerTile = 2048;
 // fp32 byte path: two voxels per lane per step, lerps packed across them
 // fp32 byte pair loop: step fraction words + one cell index per voxel
 // instead of 64-bit fixed-point coordinates
+#ifndef ER_BITS_CELLSTEP
+#define ER_BITS_CELLSTEP 1
+#endif
 #ifndef ER_PAIR_CELLSTEP
 #define ER_PAIR_CELLSTEP 1
 #endif
@@ -1085,6 +1088,67 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
         constexpr int NB = kLanes >= 8 ? ER_BITS_NB_WIDE : ER_BITS_NB;
         int ti = toff + k;
         const int ti_end = toff + qhi - (NB - 1) * kLanes;
+        const long long duN = NB * du1, dvN = NB * dv1, dwN = NB * dw1;
+        const uint8_t* __restrict__ bytes = reinterpret_cast<const uint8_t*>(oct);
+#if ER_BITS_CELLSTEP
+        // cell-index stepping (cell_step): voxel 0's fraction words + cell
+        // index step by NB voxels, voxels 1..NB-1 are chained from it by one
+        // voxel each; the samples only need the fraction words (bits_boundary's
+        // 32-bit fractions, the nearest mode's bit 31)
+        unsigned qu0 = (unsigned)cu, qv0 = (unsigned)cv, qw0 = (unsigned)cw;
+        int cell0 = (F::ipart(cu) * og.cy + F::ipart(cv)) * og.cz + F::ipart(cw);
+        const unsigned l1u = (unsigned)du1, l1v = (unsigned)dv1, l1w = (unsigned)dw1;
+        const unsigned lNu = (unsigned)duN, lNv = (unsigned)dvN, lNw = (unsigned)dwN;
+        const int h1 = F::ipart(du1) * cyz + F::ipart(dv1) * og.cz + F::ipart(dw1);
+        const int hN = F::ipart(duN) * cyz + F::ipart(dvN) * og.cz + F::ipart(dwN);
+        const int ti0 = ti;
+        for (; ti < ti_end; ti += NB * kLanes) {
+          unsigned cc[NB], wu[NB], wv[NB], ww[NB];
+          TT yy[NB];
+          const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
+          int cm = cell0;
+          wu[0] = qu0;
+          wv[0] = qv0;
+          ww[0] = qw0;
+#pragma unroll
+          for (int m = 0; m < NB; ++m) {
+            if (m > 0)
+              cm = cell_step(wu[m - 1], wv[m - 1], ww[m - 1], cm, l1u, l1v, l1w, h1, cyz, og.cz,
+                             wu[m], wv[m], ww[m]);
+            cc[m] = __ldg(bytes + (unsigned)er_idx(cm, ncells));
+            yy[m] = __ldg(tp + m * kLanes);
+          }
+#pragma unroll
+          for (int m = 0; m < NB; ++m) {
+            const auto yf = ty.add(yy[m]);
+            if (LERP == ER_LERP_NEAREST) {
+              // corner bit: fraction >= 0.5 <=> bit 31 of the fraction word
+              const unsigned bsel = (wu[m] >> 31) | ((wv[m] >> 31) << 1) | ((ww[m] >> 31) << 2);
+              if ((cc[m] >> bsel) & 1u) {
+                ++ones;
+                if (kU8Tgt) ones_y += (unsigned)yy[m];
+                else pyx += (float)yf;
+              }
+            } else if (cc[m] == 0xFFu) {
+              ++ones;
+              if (kU8Tgt) ones_y += (unsigned)yy[m];
+              else pyx += (float)yf;
+            } else if (cc[m] != 0u) {
+              bits_boundary(cc[m], (long long)wu[m], (long long)wv[m], (long long)ww[m],
+                            (double)yf, racc[threadIdx.x]);
+            }
+          }
+          cell0 = cell_step(qu0, qv0, qw0, cell0, lNu, lNv, lNw, hN, cyz, og.cz, qu0, qv0, qw0);
+        }
+        k = ti - toff;
+        {
+          // the 64-bit coordinates for the single-voxel tail
+          const long long np = (ti - ti0) / (NB * kLanes);
+          cu += np * duN;
+          cv += np * dvN;
+          cw += np * dwN;
+        }
+#else
         long long qu[NB], qv[NB], qw[NB];
 #pragma unroll
         for (int m = 0; m < NB; ++m) {
@@ -1092,8 +1156,6 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
           qv[m] = cv + m * dv1;
           qw[m] = cw + m * dw1;
         }
-        const long long duN = NB * du1, dvN = NB * dv1, dwN = NB * dw1;
-        const uint8_t* __restrict__ bytes = reinterpret_cast<const uint8_t*>(oct);
         for (; ti < ti_end; ti += NB * kLanes) {
           unsigned cc[NB];
           TT yy[NB];
@@ -1132,6 +1194,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
         cu = qu[0];
         cv = qv[0];
         cw = qw[0];
+#endif
       }
       if (kPair) {
         // two voxels per lane per step (k and k + kLanes): the fractions, the
