@@ -43,7 +43,8 @@
 //   ER_OCT_THREADS=128, ER_OCT_MINBLOCKS_F32=8   fp32-class CTA size / CTAs per SM
 //   ER_OCT_MINBLOCKS_NEAREST=10 (_BITS, _QUAD = 8)  per-path CTAs per SM
 //   ER_PAIR_CELLSTEP=1     byte pair loop: fraction words + one cell index per voxel
-//   ER_OCT_THREADS_F64=128, ER_OCT_MINBLOCKS_F64=6  the same for the fp64-lerp kernel
+//   ER_OCT_THREADS_F64=128, ER_OCT_MINBLOCKS_F64=5  the same for the fp64-lerp kernel
+//   ER_Q52_CELLSTEP=1, ER_BITS_CELLSTEP=1  cell-index stepping in the fp64 / mask loops
 //   ER_OCT_SMEM_ACC=1      per-lane fp64 group accumulators in shared memory
 //   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2 (single voxels)
 //   ER_OCT_ACC2=1          px += x; (pxx, pyx) by one FFMA2 of x * (x, y)
@@ -141,6 +142,9 @@ constexpr int kRowsPerTile = 2048;
 // fp32 byte path: two voxels per lane per step, lerps packed across them
 // fp32 byte pair loop: step fraction words + one cell index per voxel
 // instead of 64-bit fixed-point coordinates
+#ifndef ER_Q52_CELLSTEP
+#define ER_Q52_CELLSTEP 1
+#endif
 #ifndef ER_BITS_CELLSTEP
 #define ER_BITS_CELLSTEP 1
 #endif
@@ -199,7 +203,9 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 #define ER_OCT_MINBLOCKS_F32 8
 #endif
 #ifndef ER_OCT_MINBLOCKS_F64
-#define ER_OCT_MINBLOCKS_F64 (3 * 256 / ER_OCT_THREADS_F64)
+// 5 x 128 threads: 88 registers keep the fp64 pair loop's step words
+// resident (27.2 vs 28.2 ms on C2 at 6 CTAs without the cell-index stepping)
+#define ER_OCT_MINBLOCKS_F64 (5 * 128 / ER_OCT_THREADS_F64)
 #endif
 // per-path CTAs per SM: nearest-neighbour byte sampling 10 (14.6 vs 16.3 ms
 // on C2 at 8: fewer registers, more warps to hide the gathers); the bit-oct
@@ -753,8 +759,7 @@ __device__ __forceinline__ double byte_hi52(unsigned w, unsigned sel) {
 // offset exactly, every lerp result is 2^52 + value rounded to one unit
 // (2^-41 byte), and the offset is removed once at the end -- one DADD instead
 // of one per base corner.
-__device__ __forceinline__ double lerp_q52(uint2 c8, long long cu, long long cv, long long cw) {
-  const double fu = q52_frac(cu), fv = q52_frac(cv), fw = q52_frac(cw);
+__device__ __forceinline__ double lerp_q52f(uint2 c8, double fu, double fv, double fw) {
   const double m000 = byte_hi52(c8.x, 0), m100 = byte_hi52(c8.x, 1);
   const double m010 = byte_hi52(c8.x, 2), m110 = byte_hi52(c8.x, 3);
   const double m001 = byte_hi52(c8.y, 0), m101 = byte_hi52(c8.y, 1);
@@ -766,6 +771,49 @@ __device__ __forceinline__ double lerp_q52(uint2 c8, long long cu, long long cv,
   const double c0 = fma(fv, c10 - c00, c00);
   const double c1 = fma(fv, c11 - c01, c01);
   return fma(fw, c1 - c0, c0) - 4503599627370496.0;
+}
+__device__ __forceinline__ double lerp_q52(uint2 c8, long long cu, long long cv, long long cw) {
+  return lerp_q52f(c8, q52_frac(cu), q52_frac(cv), q52_frac(cw));
+}
+
+// Q12.52 coordinates as (64-bit fraction words, padded cell index) for the
+// fp64 pair loop (ER_Q52_CELLSTEP): the 52 fraction bits shifted to the top
+// of a 64-bit word, so fraction carries are the hardware carries.
+__device__ __forceinline__ void q52_split(long long q, unsigned& lo, unsigned& hi) {
+  const unsigned long long f = (unsigned long long)q << 12;
+  lo = (unsigned)f;
+  hi = (unsigned)(f >> 32);
+}
+// exact double of the fraction: its 52 bits are the mantissa of 1 + f
+__device__ __forceinline__ double q64_frac(unsigned lo, unsigned hi) {
+  return __hiloint2double((int)((hi >> 12) | 0x3FF00000u), (int)__funnelshift_r(lo, hi, 12)) -
+         1.0;
+}
+// one step: 64-bit fraction words + 64-bit step words (explicit PTX carry
+// chains), the cell index moved by h plus the strides of the carried axes
+__device__ __forceinline__ int cell_step64(const unsigned (&a)[6], int cell, const unsigned (&d)[6],
+                                           int h, int cyz, int cz, unsigned (&o)[6]) {
+  int out;
+  asm("{\n\t.reg .u32 fu, fv;\n\t.reg .pred pu, pv;\n\t"
+      "add.cc.u32 %0, %7, %13;\n\t"
+      "addc.cc.u32 %1, %8, %14;\n\t"
+      "addc.u32 fu, 0, 0;\n\t"
+      "add.cc.u32 %2, %9, %15;\n\t"
+      "addc.cc.u32 %3, %10, %16;\n\t"
+      "addc.u32 fv, 0, 0;\n\t"
+      "add.cc.u32 %4, %11, %17;\n\t"
+      "addc.cc.u32 %5, %12, %18;\n\t"
+      "addc.u32 %6, %19, %20;\n\t"
+      "setp.ne.u32 pu, fu, 0;\n\t"
+      "setp.ne.u32 pv, fv, 0;\n\t"
+      "selp.u32 fu, %21, 0, pu;\n\t"
+      "selp.u32 fv, %22, 0, pv;\n\t"
+      "add.u32 %6, %6, fu;\n\t"
+      "add.u32 %6, %6, fv;\n\t}"
+      : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(out)
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(d[0]), "r"(d[1]),
+        "r"(d[2]), "r"(d[3]), "r"(d[4]), "r"(d[5]), "r"(cell), "r"(h), "r"(cyz), "r"(cz));
+  return out;
 }
 
 // fp32 trilinear sample from two quad entries (planes k0, k1), each
@@ -1011,6 +1059,50 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
         // scale (lerp_q52), removed exactly when the group is folded
         int ti = toff + k;
         const int ti_end = toff + qhi - kLanes;
+#if ER_Q52_CELLSTEP
+        // cell-index stepping with 64-bit fraction words (cell_step64);
+        // bit-identical to the Q12.52 arithmetic below
+        unsigned a[6], d1[6], d2[6];
+        q52_split(cu, a[0], a[1]);
+        q52_split(cv, a[2], a[3]);
+        q52_split(cw, a[4], a[5]);
+        q52_split(du1, d1[0], d1[1]);
+        q52_split(dv1, d1[2], d1[3]);
+        q52_split(dw1, d1[4], d1[5]);
+        q52_split(du2, d2[0], d2[1]);
+        q52_split(dv2, d2[2], d2[3]);
+        q52_split(dw2, d2[4], d2[5]);
+        int cella = (q52_ipart(cu) * og.cy + q52_ipart(cv)) * og.cz + q52_ipart(cw);
+        const int h1 = q52_ipart(du1) * cyz + q52_ipart(dv1) * og.cz + q52_ipart(dw1);
+        const int h2 = q52_ipart(du2) * cyz + q52_ipart(dv2) * og.cz + q52_ipart(dw2);
+        const int ti0 = ti;
+        for (; ti < ti_end; ti += 2 * kLanes) {
+          unsigned b[6];
+          const int cellb = cell_step64(a, cella, d1, h1, cyz, og.cz, b);
+          const uint2 a8 = ld_oct(oct + (unsigned)er_idx(cella, ncells));
+          const uint2 b8 = ld_oct(oct + (unsigned)er_idx(cellb, ncells));
+          const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
+          const double ya = (double)ty.add(__ldg(tp));
+          const double yb = (double)ty.add(__ldg(tp + kLanes));
+          const double xa = lerp_q52f(a8, q64_frac(a[0], a[1]), q64_frac(a[2], a[3]),
+                                      q64_frac(a[4], a[5]));
+          const double xb = lerp_q52f(b8, q64_frac(b[0], b[1]), q64_frac(b[2], b[3]),
+                                      q64_frac(b[4], b[5]));
+          qx += xa;
+          qxx = fma(xa, xa, qxx);
+          qyx = fma(ya, xa, qyx);
+          qx += xb;
+          qxx = fma(xb, xb, qxx);
+          qyx = fma(yb, xb, qyx);
+          cella = cell_step64(a, cella, d2, h2, cyz, og.cz, a);
+        }
+        {
+          const long long np = (ti - ti0) / (2 * kLanes);
+          cu += np * du2;
+          cv += np * dv2;
+          cw += np * dw2;
+        }
+#else
         long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
         for (; ti < ti_end; ti += 2 * kLanes) {
           const int ca = (q52_ipart(cu) * og.cy + q52_ipart(cv)) * og.cz + q52_ipart(cw);
@@ -1035,6 +1127,7 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
           bv += dv2;
           bw += dw2;
         }
+#endif
         if (ti < toff + qhi) {  // this lane's last voxel, unpaired
           const int ca = (q52_ipart(cu) * og.cy + q52_ipart(cv)) * og.cz + q52_ipart(cw);
           const uint2 a8 = ld_oct(oct + (unsigned)er_idx(ca, ncells));
