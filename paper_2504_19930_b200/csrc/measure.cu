@@ -42,9 +42,7 @@
 //   ER_REFINE=1            fp64 refinement of ill-conditioned f32 particles
 //   ER_OCT_THREADS=128, ER_OCT_MINBLOCKS_F32=8   fp32-class CTA size / CTAs per SM
 //   ER_OCT_MINBLOCKS_NEAREST=10 (_BITS, _QUAD = 8)  per-path CTAs per SM
-//   ER_PAIR_CELLSTEP=1     byte pair loop: fraction words + one cell index per voxel
 //   ER_OCT_THREADS_F64=128, ER_OCT_MINBLOCKS_F64=5  the same for the fp64-lerp kernel
-//   ER_Q52_CELLSTEP=1, ER_BITS_CELLSTEP=1  cell-index stepping in the fp64 / mask loops
 //   ER_OCT_SMEM_ACC=1      per-lane fp64 group accumulators in shared memory
 //   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2 (single voxels)
 //   ER_OCT_ACC2=1          px += x; (pxx, pyx) by one FFMA2 of x * (x, y)
@@ -53,7 +51,6 @@
 //   ER_FRAC_RN=1           ... rounded to nearest (0: truncated, biased low)
 //   ER_OCT_TILE_MAJOR=1    tile-major CTA order (0: particle-major)
 //   ER_OCT_UNROLL=1        voxel-loop unroll; ER_OCT_LDPOLICY=0 (.nc; 1 .cg, 2 .cs)
-//   ER_OPAQUE_STEP=0       pair-loop steps held in opaque registers (rejected)
 //   ER_MIN_TILES=8         minimum tiles per particle
 //   ER_BOUNDS_CHECK=0      debug build: every gather index range-checked (common.cuh)
 #include <type_traits>
@@ -122,14 +119,6 @@ constexpr int kRowsPerTile = 2048;
 #ifndef ER_OCT_LANES_NEAREST
 #define ER_OCT_LANES_NEAREST (ER_OCT_HALF ? 8 : 32)
 #endif
-// perf-only experiments on the pair loop's target loads (see above); never set
-// in a real build
-#ifndef ER_EXP_TGT
-#define ER_EXP_TGT 0
-#endif
-#ifndef ER_OPAQUE_STEP
-#define ER_OPAQUE_STEP 0
-#endif
 // two of the eight corner conversions of the pair loop on the XU pipe
 #ifndef ER_CORNER_XU
 #define ER_CORNER_XU 1
@@ -140,17 +129,6 @@ constexpr int kRowsPerTile = 2048;
 #endif
 
 // fp32 byte path: two voxels per lane per step, lerps packed across them
-// fp32 byte pair loop: step fraction words + one cell index per voxel
-// instead of 64-bit fixed-point coordinates
-#ifndef ER_Q52_CELLSTEP
-#define ER_Q52_CELLSTEP 1
-#endif
-#ifndef ER_BITS_CELLSTEP
-#define ER_BITS_CELLSTEP 1
-#endif
-#ifndef ER_PAIR_CELLSTEP
-#define ER_PAIR_CELLSTEP 1
-#endif
 #ifndef ER_OCT_PAIR
 #define ER_OCT_PAIR 1
 #endif
@@ -562,7 +540,7 @@ __device__ __forceinline__ double byte_m64(unsigned w, unsigned sel) {
 }
 
 
-// One step of the cell-index coordinates (ER_PAIR_CELLSTEP): fraction words
+// One step of the cell-index coordinates (the pair and mask loops): fraction words
 // (u, v, w) + (lu, lv, lw) with the carries as explicit PTX carry chains; the
 // cell index moves by h (the step's integer parts times the strides) plus
 // cyz / cz / 1 for each carried axis.
@@ -777,7 +755,7 @@ __device__ __forceinline__ double lerp_q52(uint2 c8, long long cu, long long cv,
 }
 
 // Q12.52 coordinates as (64-bit fraction words, padded cell index) for the
-// fp64 pair loop (ER_Q52_CELLSTEP): the 52 fraction bits shifted to the top
+// fp64 pair loop: the 52 fraction bits shifted to the top
 // of a 64-bit word, so fraction carries are the hardware carries.
 __device__ __forceinline__ void q52_split(long long q, unsigned& lo, unsigned& hi) {
   const unsigned long long f = (unsigned long long)q << 12;
@@ -981,13 +959,6 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
   constexpr bool kPairQuad = ER_OCT_PAIR_QUAD && kQuad;
   const long long du1 = kLanes * du, dv1 = kLanes * dv, dw1 = kLanes * dw;
   long long du2 = 2 * du1, dv2 = 2 * dv1, dw2 = 2 * dw1;
-#if ER_OPAQUE_STEP
-  // keep the per-iteration steps in registers (else ptxas re-derives them
-  // from du with LEA shift-adds on the ALU pipe)
-  asm volatile("mov.b64 %0, %0;" : "+l"(du2));
-  asm volatile("mov.b64 %0, %0;" : "+l"(dv2));
-  asm volatile("mov.b64 %0, %0;" : "+l"(dw2));
-#endif
 
   for (int grp = warp; grp < ngroups;) {
     const int r = grp * 32 + lane;
@@ -1059,9 +1030,9 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
         // scale (lerp_q52), removed exactly when the group is folded
         int ti = toff + k;
         const int ti_end = toff + qhi - kLanes;
-#if ER_Q52_CELLSTEP
         // cell-index stepping with 64-bit fraction words (cell_step64);
-        // bit-identical to the Q12.52 arithmetic below
+        // bit-identical to plain Q12.52 arithmetic (the low 12 bits of the
+        // fraction words stay 0)
         unsigned a[6], d1[6], d2[6];
         q52_split(cu, a[0], a[1]);
         q52_split(cv, a[2], a[3]);
@@ -1102,32 +1073,6 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
           cv += np * dv2;
           cw += np * dw2;
         }
-#else
-        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
-        for (; ti < ti_end; ti += 2 * kLanes) {
-          const int ca = (q52_ipart(cu) * og.cy + q52_ipart(cv)) * og.cz + q52_ipart(cw);
-          const int cb = (q52_ipart(bu) * og.cy + q52_ipart(bv)) * og.cz + q52_ipart(bw);
-          const uint2 a8 = ld_oct(oct + (unsigned)er_idx(ca, ncells));
-          const uint2 b8 = ld_oct(oct + (unsigned)er_idx(cb, ncells));
-          const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
-          const double ya = (double)ty.add(__ldg(tp));
-          const double yb = (double)ty.add(__ldg(tp + kLanes));
-          const double xa = lerp_q52(a8, cu, cv, cw);
-          const double xb = lerp_q52(b8, bu, bv, bw);
-          qx += xa;
-          qxx = fma(xa, xa, qxx);
-          qyx = fma(ya, xa, qyx);
-          qx += xb;
-          qxx = fma(xb, xb, qxx);
-          qyx = fma(yb, xb, qyx);
-          cu += du2;
-          cv += dv2;
-          cw += dw2;
-          bu += du2;
-          bv += dv2;
-          bw += dw2;
-        }
-#endif
         if (ti < toff + qhi) {  // this lane's last voxel, unpaired
           const int ca = (q52_ipart(cu) * og.cy + q52_ipart(cv)) * og.cz + q52_ipart(cw);
           const uint2 a8 = ld_oct(oct + (unsigned)er_idx(ca, ncells));
@@ -1183,7 +1128,6 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
         const int ti_end = toff + qhi - (NB - 1) * kLanes;
         const long long duN = NB * du1, dvN = NB * dv1, dwN = NB * dw1;
         const uint8_t* __restrict__ bytes = reinterpret_cast<const uint8_t*>(oct);
-#if ER_BITS_CELLSTEP
         // cell-index stepping (cell_step): voxel 0's fraction words + cell
         // index step by NB voxels, voxels 1..NB-1 are chained from it by one
         // voxel each; the samples only need the fraction words (bits_boundary's
@@ -1241,53 +1185,6 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
           cv += np * dvN;
           cw += np * dwN;
         }
-#else
-        long long qu[NB], qv[NB], qw[NB];
-#pragma unroll
-        for (int m = 0; m < NB; ++m) {
-          qu[m] = cu + m * du1;
-          qv[m] = cv + m * dv1;
-          qw[m] = cw + m * dw1;
-        }
-        for (; ti < ti_end; ti += NB * kLanes) {
-          unsigned cc[NB];
-          TT yy[NB];
-          const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
-#pragma unroll
-          for (int m = 0; m < NB; ++m) {
-            const int cm = (F::ipart(qu[m]) * og.cy + F::ipart(qv[m])) * og.cz + F::ipart(qw[m]);
-            cc[m] = __ldg(bytes + (unsigned)er_idx(cm, ncells));
-            yy[m] = __ldg(tp + m * kLanes);
-          }
-#pragma unroll
-          for (int m = 0; m < NB; ++m) {
-            const auto yf = ty.add(yy[m]);
-            if (LERP == ER_LERP_NEAREST) {
-              // corner bit: fraction >= 0.5 <=> bit 31 of the fixed-point word
-              const unsigned bsel = ((unsigned)qu[m] >> 31) | (((unsigned)qv[m] >> 31) << 1) |
-                                    (((unsigned)qw[m] >> 31) << 2);
-              if ((cc[m] >> bsel) & 1u) {
-                ++ones;
-                if (kU8Tgt) ones_y += (unsigned)yy[m];
-                else pyx += (float)yf;
-              }
-            } else if (cc[m] == 0xFFu) {
-              ++ones;
-              if (kU8Tgt) ones_y += (unsigned)yy[m];
-              else pyx += (float)yf;
-            } else if (cc[m] != 0u) {
-              bits_boundary(cc[m], qu[m], qv[m], qw[m], (double)yf, racc[threadIdx.x]);
-            }
-            qu[m] += duN;
-            qv[m] += dvN;
-            qw[m] += dwN;
-          }
-        }
-        k = ti - toff;
-        cu = qu[0];
-        cv = qv[0];
-        cw = qw[0];
-#endif
       }
       if (kPair) {
         // two voxels per lane per step (k and k + kLanes): the fractions, the
@@ -1301,7 +1198,6 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
         // loop test and the target address
         int ti = toff + k;
         const int ti_end = toff + qhi - kLanes;
-#if ER_PAIR_CELLSTEP
         // cell-index stepping: the fixed-point coordinates live as their
         // 32-bit fraction words plus ONE padded cell index per voxel; a step
         // adds the fraction words (the carries are the integer parts'
@@ -1340,47 +1236,6 @@ __global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>:
           cv += np * dv2;
           cw += np * dw2;
         }
-#else
-        // voxel b = voxel a + kLanes along the row: its own coordinate set,
-        // both stepped by 2 kLanes per iteration
-        long long bu = cu + du1, bv = cv + dv1, bw = cw + dw1;
-
-        for (; ti < ti_end; ti += 2 * kLanes) {
-          // Horner form: two IMADs per cell index
-          const int ca = (F::ipart(cu) * og.cy + F::ipart(cv)) * og.cz + F::ipart(cw);
-          const int cb = (F::ipart(bu) * og.cy + F::ipart(bv)) * og.cz + F::ipart(bw);
-          const uint2 a8 = ld_oct(oct + (unsigned)er_idx(ca, ncells));
-          const uint2 b8 = ld_oct(oct + (unsigned)er_idx(cb, ncells));
-          const TT* tp = tgt + (unsigned)er_idx(ti, ntv);
-#if ER_EXP_TGT == 1
-          // perf-only experiment (wrong numbers): voxel b reuses voxel a's
-          // target value -- bounds what sharing a target load between two
-          // samples (e.g. two particles per CTA) could save
-          const TT ya = __ldg(tp);
-          const TT yb = ya;
-#elif ER_EXP_TGT == 2
-          // perf-only experiment (wrong numbers): no target loads at all
-          const TT ya = (TT)(ti & 7), yb = (TT)(ti & 3);
-#else
-          const TT ya = __ldg(tp);
-          const TT yb = __ldg(tp + kLanes);
-#endif
-          const float2 y2 = tgt_add2(ty, ya, yb);
-          const float2 fu = __fmul2_rn(make_float2(ER_U2F((unsigned)cu), ER_U2F((unsigned)bu)), sc);
-          const float2 fv = __fmul2_rn(make_float2(ER_U2F((unsigned)cv), ER_U2F((unsigned)bv)), sc);
-          const float2 fw = __fmul2_rn(make_float2(ER_U2F((unsigned)cw), ER_U2F((unsigned)bw)), sc);
-          const float2 x = lerp_oct_f32x2(a8, b8, fu, fv, fw);
-          sx2 = __fadd2_rn(sx2, x);
-          sxx2 = __ffma2_rn(x, x, sxx2);
-          syx2 = __ffma2_rn(x, y2, syx2);
-          cu += du2;
-          cv += dv2;
-          cw += dw2;
-          bu += du2;
-          bv += dv2;
-          bw += dw2;
-        }
-#endif
         k = ti - toff;
         px = sx2.x + sx2.y;
         pxx = sxx2.x + sxx2.y;
