@@ -41,7 +41,7 @@
 //   ER_F64_Q52=1           fp64-lerp mode: Q12.52 coordinates + voxel pairs
 //   ER_REFINE=1            fp64 refinement of ill-conditioned f32 particles
 //   ER_OCT_THREADS=128, ER_OCT_MINBLOCKS_F32=8   fp32-class CTA size / CTAs per SM
-//   ER_OCT_MINBLOCKS_NEAREST=10 (_BITS, _QUAD = 8)  per-path CTAs per SM
+//   ER_OCT_MINBLOCKS_NEAREST=10, _F32_OVL=7 (_BITS, _QUAD = 8)  per-path CTAs per SM
 //   ER_OCT_THREADS_F64=128, ER_OCT_MINBLOCKS_F64=5  the same for the fp64-lerp kernel
 //   ER_OCT_SMEM_ACC=1      per-lane fp64 group accumulators in shared memory
 //   ER_OCT_FMUL2=1         u/v fraction scaling as one packed FMUL2 (single voxels)
@@ -196,6 +196,11 @@ __device__ __forceinline__ uint2 ld_oct(const uint2* p) {
 #endif
 #ifndef ER_OCT_MINBLOCKS_QUAD
 #define ER_OCT_MINBLOCKS_QUAD ER_OCT_MINBLOCKS_F32
+#endif
+// the overlap-region fp32 byte kernel (the extra target sum of squares) at 7:
+// 72 registers let ptxas issue both target loads early (19.2 vs 20.2 ms on C2)
+#ifndef ER_OCT_MINBLOCKS_F32_OVL
+#define ER_OCT_MINBLOCKS_F32_OVL 7
 #endif
 #ifndef ER_MIN_TILES
 #define ER_MIN_TILES 8
@@ -859,17 +864,18 @@ struct OctLanes {
                                                      : ER_OCT_LANES;
 };
 
-template <int LERP, int BITS>
+template <int LERP, int BITS, int OVL>
 struct OctMinBlocks {
   static constexpr int n = LERP == ER_LERP_F64 ? ER_OCT_MINBLOCKS_F64
                            : BITS == 1         ? ER_OCT_MINBLOCKS_BITS
                            : BITS == 2         ? ER_OCT_MINBLOCKS_QUAD
                            : LERP == ER_LERP_NEAREST ? ER_OCT_MINBLOCKS_NEAREST
+                           : OVL                     ? ER_OCT_MINBLOCKS_F32_OVL
                                                      : ER_OCT_MINBLOCKS_F32;
 };
 
 template <typename TT, int LERP, int BITS, int OVL, int LN = 0>
-__global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS>::n)
+__global__ void __launch_bounds__(OctThreads<LERP>::n, OctMinBlocks<LERP, BITS, OVL>::n)
     measure_oct_kernel(const TT* __restrict__ tgt, const uint2* __restrict__ oct,
                        const double* __restrict__ A, const double* __restrict__ B, const Geom g,
                        const OctGeom og, Partial* __restrict__ part) {

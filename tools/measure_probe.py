@@ -1,6 +1,7 @@
 """Dev probe: measurement-kernel throughput on the C2 workload (CUDA events
 on the launching stream).  usage: measure_probe.py [P] [precisions] [reps]
-(ER_PROBE_MODE=mask: the binary masks of the same pair)"""
+(ER_PROBE_MODE=mask: the binary masks of the same pair; ER_PROBE_OVERLAP=1:
+the overlap region)"""
 import json
 import os
 import sys
@@ -29,15 +30,16 @@ run = dsmc.DeviceSmcRun(t, s, cfg, Executor())
 run.predict(0)
 A, B = run.A[:P], run.B[:P]
 nvox = t.data.size
+ovl = os.environ.get("ER_PROBE_OVERLAP", "0") == "1"
 res = {}
 for prec in precs:
     for _ in range(2):
-        z, d, n = ops.measure(run.tdv, run.sdv, A, B, False, prec)
+        z, d, n = ops.measure(run.tdv, run.sdv, A, B, ovl, prec)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        z, d, n = ops.measure(run.tdv, run.sdv, A, B, False, prec)
+        z, d, n = ops.measure(run.tdv, run.sdv, A, B, ovl, prec)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
