@@ -213,9 +213,13 @@ int er_argmax_update(const double *z_dev, int64_t n, int64_t base_index, double 
 /* One SMC update after measurement: best tracking (smc.py:203-206),
  * update_weights (210-224), ess (227-229), resample_systematic with stream
  * (seed, 2, k, 0) when ess < ess_fraction * n (232-248, 353-357), estimate
- * (251-259) and the trace row (358-364).  Single CTA, no host round trip.
- * ctl_dev layout: see er_smc_ctl below.  weights_dev is updated in place;
- * states_out/z_out receive the (possibly resampled) population. */
+ * (251-259) and the trace row (358-364).  No host round trip: one CTA for
+ * n < 16384, else a chain of whole-GPU kernels with the same per-chunk loops
+ * and reduction trees (bit-identical results).  ctl_dev layout: see
+ * er_smc_ctl below.  weights_dev is updated in place; states_out/z_out
+ * receive the (possibly resampled) population; z_out, states_out and
+ * scratch must not alias the inputs (z_out and scratch also serve as the
+ * large-n path's reduction scratch). */
 typedef struct er_smc_ctl {
   double best_measurement; /* running best (init -1.0) */
   double best_state[6];

@@ -1,6 +1,8 @@
 // SMC particle machinery on device (reference: echoreg/smc.py:145-259,
 // geometry.py:76-152, exhaustive.py:25-113).  Everything between two
 // measurements runs here, so an SMC iteration never round-trips to the host.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "rng.cuh"
 
@@ -420,6 +422,292 @@ __global__ void __launch_bounds__(kUpdThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// The same update for large populations (n >= kMultiMin) spread over the whole
+// GPU.  The single-CTA kernel above is bound by one SM's latency and
+// bandwidth at 10^5 particles (7 ms at 262,144: the binary searches of the
+// resampling walk a global CDF).  Here every phase keeps EXACTLY the
+// single-CTA numerics -- the same 1024 contiguous per-thread chunks
+// (chunk = ceil(n / 1024)), the same sequential per-chunk loops, the same
+// fixed-order trees over the 1024 chunk partials (block_sum, block_sum_n,
+// block_argmax, block_exclusive_scan run by one 1024-thread CTA on the
+// partials) -- so the results are bit-identical; only the per-element work
+// (weights, searchsorted, gathers) runs on all SMs.  No extra memory: the
+// chunk partials live in z_out (phases before the resampling writes it) and
+// in scratch (after the CDF is consumed), the scalars in the trace row
+// (rewritten by the last phase).  Requires n >= kMultiMin (partial space).
+// ---------------------------------------------------------------------------
+constexpr long long kMultiMin = 16384;
+constexpr int kChunkThreads = 128;  // chunk kernels: 8 CTAs x 128 = 1024 chunks
+// trace-row slots used as scalar scratch until the final phase rewrites them
+enum { kTrM = 0, kTrTotal = 1, kTrReset = 2, kTrEss = 9, kTrFire = 10, kTrNdeg = 11 };
+
+__device__ __forceinline__ void chunk_range(long long n, long long& lo, long long& hi) {
+  const long long c = (long long)blockIdx.x * kChunkThreads + threadIdx.x;
+  const long long chunk = (n + kUpdThreads - 1) / kUpdThreads;
+  lo = min(n, c * chunk);
+  hi = min(n, lo + chunk);
+}
+
+// phase 1: per-chunk best (value, index) and degenerate count
+template <typename ZA>
+__global__ void __launch_bounds__(kChunkThreads) upd_best_chunks(const ZA za, long long n,
+                                                                 double* __restrict__ part) {
+  long long lo, hi;
+  chunk_range(n, lo, hi);
+  double bv = -INFINITY;
+  long long bi = 1LL << 62;
+  double ndeg = 0.0;
+  for (long long i = lo; i < hi; ++i) {
+    better(bv, bi, za.zv(i), i);
+    ndeg += za.dg(i);
+  }
+  const int c = blockIdx.x * kChunkThreads + threadIdx.x;
+  part[c] = bv;
+  reinterpret_cast<long long*>(part)[kUpdThreads + c] = bi;
+  part[2 * kUpdThreads + c] = ndeg;  // kept until phase 5
+}
+
+// phase 2 (one CTA): best tracking and the weight exponent offset
+__global__ void __launch_bounds__(kUpdThreads)
+    upd_best_reduce(const double* __restrict__ part, const double* __restrict__ st_in,
+                    double beta, er_smc_ctl* __restrict__ ctl, double* __restrict__ trace) {
+  __shared__ double shv[40];
+  __shared__ long long shi[40];
+  double bv = part[threadIdx.x];
+  long long bi = reinterpret_cast<const long long*>(part)[kUpdThreads + threadIdx.x];
+  block_argmax(bv, bi, shv, shi);
+  if (threadIdx.x == 0) {
+    if (bv > ctl->best_measurement) {
+      ctl->best_measurement = bv;
+      ctl->has_best = 1;
+      for (int d = 0; d < 6; ++d) ctl->best_state[d] = st_in[6 * bi + d];
+    }
+    trace[kTrM] = rn_mul(beta, bv);
+  }
+}
+
+// phase 3: w *= exp(beta z - m), per-chunk sums
+template <typename ZA>
+__global__ void __launch_bounds__(kChunkThreads)
+    upd_weight_chunks(const ZA za, double* __restrict__ w, long long n, double beta,
+                      const double* __restrict__ trace, double* __restrict__ part) {
+  long long lo, hi;
+  chunk_range(n, lo, hi);
+  const double m = trace[kTrM];
+  double s = 0.0;
+  for (long long i = lo; i < hi; ++i) {
+    const double wi = rn_mul(w[i], exp(rn_sub(rn_mul(beta, za.zv(i)), m)));
+    w[i] = wi;
+    s += wi;
+  }
+  part[3 * kUpdThreads + blockIdx.x * kChunkThreads + threadIdx.x] = s;
+}
+
+// phase 4 (one CTA): the weight total
+__global__ void __launch_bounds__(kUpdThreads) upd_total_reduce(const double* __restrict__ part,
+                                                                double* __restrict__ trace) {
+  __shared__ double sh[33];
+  const double total = block_sum(part[3 * kUpdThreads + threadIdx.x], sh);
+  if (threadIdx.x == 0) {
+    trace[kTrTotal] = total;
+    trace[kTrReset] = (!isfinite(total) || total <= 0.0) ? 1.0 : 0.0;
+  }
+}
+
+// phase 5: normalise, per-chunk (sum w, sum w^2)
+__global__ void __launch_bounds__(kChunkThreads)
+    upd_norm_chunks(double* __restrict__ w, long long n, const double* __restrict__ trace,
+                    double* __restrict__ part) {
+  long long lo, hi;
+  chunk_range(n, lo, hi);
+  const double total = trace[kTrTotal];
+  const bool reset = trace[kTrReset] != 0.0;
+  double part2 = 0.0, psum = 0.0;
+  for (long long i = lo; i < hi; ++i) {
+    const double wi = reset ? rn_div(1.0, (double)n) : rn_div(w[i], total);
+    w[i] = wi;
+    part2 = fma(wi, wi, part2);
+    psum += wi;
+  }
+  const int c = blockIdx.x * kChunkThreads + threadIdx.x;
+  part[4 * kUpdThreads + c] = psum;
+  part[5 * kUpdThreads + c] = part2;
+}
+
+// phase 6 (one CTA): ESS and the resampling decision
+__global__ void __launch_bounds__(kUpdThreads)
+    upd_ess_reduce(const double* __restrict__ part, long long n, double ess_frac,
+                   er_smc_ctl* __restrict__ ctl, double* __restrict__ trace) {
+  __shared__ double sh[33 * 3];
+  double r3[3] = {part[4 * kUpdThreads + threadIdx.x], part[5 * kUpdThreads + threadIdx.x],
+                  part[2 * kUpdThreads + threadIdx.x]};
+  block_sum_n(r3, sh);
+  if (threadIdx.x == 0) {
+    const double ess = rn_div(1.0, r3[1]);
+    if (fabs(r3[0] - 1.0) > 1e-9) ctl->error = ER_EWEIGHTS;
+    trace[kTrEss] = ess;
+    trace[kTrFire] = ess < rn_mul(ess_frac, (double)n) ? 1.0 : 0.0;
+    trace[kTrNdeg] = r3[2];
+  }
+}
+
+// phase 7: per-chunk weight sums for the CDF (only when resampling)
+__global__ void __launch_bounds__(kChunkThreads)
+    upd_cdf_chunks(const double* __restrict__ w, long long n, const double* __restrict__ trace,
+                   double* __restrict__ part) {
+  if (trace[kTrFire] == 0.0) return;
+  long long lo, hi;
+  chunk_range(n, lo, hi);
+  double run = 0.0;
+  for (long long i = lo; i < hi; ++i) run += w[i];
+  part[6 * kUpdThreads + blockIdx.x * kChunkThreads + threadIdx.x] = run;
+}
+
+// phase 8 (one CTA): exclusive scan of the chunk sums
+__global__ void __launch_bounds__(kUpdThreads) upd_cdf_scan(double* __restrict__ part,
+                                                            const double* __restrict__ trace) {
+  __shared__ double sh[33];
+  if (trace[kTrFire] == 0.0) return;
+  const double off = block_exclusive_scan(part[6 * kUpdThreads + threadIdx.x], sh);
+  part[7 * kUpdThreads + threadIdx.x] = off;
+}
+
+// phase 9: the CDF itself (sequential within each chunk, from its offset)
+__global__ void __launch_bounds__(kChunkThreads)
+    upd_cdf_fill(const double* __restrict__ w, long long n, const double* __restrict__ trace,
+                 const double* __restrict__ part, double* __restrict__ cdf) {
+  if (trace[kTrFire] == 0.0) return;
+  long long lo, hi;
+  chunk_range(n, lo, hi);
+  double acc = part[7 * kUpdThreads + blockIdx.x * kChunkThreads + threadIdx.x];
+  for (long long i = lo; i < hi; ++i) {
+    acc += w[i];
+    cdf[i] = acc;
+  }
+}
+
+// phase 10 (one thread per particle): systematic resampling or plain copy
+template <typename ZA>
+__global__ void __launch_bounds__(256)
+    upd_resample(const ZA za, double* __restrict__ w, const double* __restrict__ st_in,
+                 double* __restrict__ st_out, double* __restrict__ z_out,
+                 const double* __restrict__ cdf, long long n, uint64_t seed, long long k,
+                 const double* __restrict__ trace) {
+  const long long i = blockIdx.x * 256LL + threadIdx.x;
+  if (i >= n) return;
+  if (trace[kTrFire] != 0.0) {
+    ErPhilox s;
+    er_stream_init(&s, seed, 2, (uint64_t)k, 0);
+    const double inv_n = rn_div(1.0, (double)n);
+    const double u0 = er_uniform(&s, 0.0, inv_n);
+    const double pos = rn_add(u0, rn_div((double)i, (double)n));
+    long long a = 0, b = n;
+    while (a < b) {
+      const long long mid = (a + b) >> 1;
+      if (cdf[mid] <= pos) a = mid + 1;
+      else b = mid;
+    }
+    const long long idx = a < n - 1 ? a : n - 1;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) st_out[6 * i + d] = st_in[6 * idx + d];
+    z_out[i] = za.zv(idx);
+  } else {
+#pragma unroll
+    for (int d = 0; d < 6; ++d) st_out[6 * i + d] = st_in[6 * i + d];
+    z_out[i] = za.zv(i);
+  }
+}
+
+// phase 11: uniform weights after resampling (all CDF reads are done)
+__global__ void __launch_bounds__(256) upd_reset_weights(double* __restrict__ w, long long n,
+                                                         const double* __restrict__ trace) {
+  const long long i = blockIdx.x * 256LL + threadIdx.x;
+  if (i < n && trace[kTrFire] != 0.0) w[i] = rn_div(1.0, (double)n);
+}
+
+// phase 12: per-chunk estimate partials (weighted state sums, z sum, z max)
+__global__ void __launch_bounds__(kChunkThreads)
+    upd_est_chunks(const double* __restrict__ w, const double* __restrict__ st_out,
+                   const double* __restrict__ z_out, long long n, double* __restrict__ part) {
+  long long lo, hi;
+  chunk_range(n, lo, hi);
+  const int c = blockIdx.x * kChunkThreads + threadIdx.x;
+  for (int d = 0; d < 6; ++d) {
+    double e = 0.0;
+    for (long long i = lo; i < hi; ++i) e = fma(w[i], st_out[6 * i + d], e);
+    part[d * kUpdThreads + c] = e;
+  }
+  double zs = 0.0, zmax = -INFINITY;
+  long long zi = 0;
+  for (long long i = lo; i < hi; ++i) {
+    zs += z_out[i];
+    better(zmax, zi, z_out[i], i);
+  }
+  part[6 * kUpdThreads + c] = zs;
+  part[7 * kUpdThreads + c] = zmax;
+  reinterpret_cast<long long*>(part)[8 * kUpdThreads + c] = zi;
+}
+
+// phase 13 (one CTA): the estimate and the trace row
+__global__ void __launch_bounds__(kUpdThreads)
+    upd_est_reduce(const double* __restrict__ part, long long n, int est_best,
+                   const er_smc_ctl* __restrict__ ctl, double* __restrict__ trace) {
+  __shared__ double sh[33 * 7];
+  __shared__ double shv[40];
+  __shared__ long long shi[40];
+  const int t = threadIdx.x;
+  double est[7];
+#pragma unroll
+  for (int d = 0; d < 7; ++d) est[d] = part[d * kUpdThreads + t];
+  block_sum_n(est, sh);
+  double zmax = part[7 * kUpdThreads + t];
+  long long zi = reinterpret_cast<const long long*>(part)[8 * kUpdThreads + t];
+  block_argmax(zmax, zi, shv, shi);
+  if (t == 0) {
+    const bool use_best = est_best && ctl->has_best;
+    for (int d = 0; d < 6; ++d) trace[d] = use_best ? ctl->best_state[d] : est[d];
+    trace[6] = rn_div(est[6], (double)n);
+    trace[7] = zmax;
+    trace[8] = ctl->best_measurement;
+    // trace[9..11] (ess, fired, n_degenerate) were written by phase 6
+  }
+}
+
+template <typename ZA>
+void smc_update_multi(const ZA& za, double* w, const double* st_in, double* st_out,
+                      double* z_out, double* scratch, long long n, double beta,
+                      double ess_frac, uint64_t seed, long long k, int est_best,
+                      er_smc_ctl* ctl, double* trace, cudaStream_t st) {
+  const unsigned cb = kUpdThreads / kChunkThreads;
+  const unsigned pb = (unsigned)((n + 255) / 256);
+  double* pre = z_out;     // partials before the resampling writes z_out
+  double* post = scratch;  // partials after the CDF has been consumed
+  upd_best_chunks<ZA><<<cb, kChunkThreads, 0, st>>>(za, n, pre);
+  upd_best_reduce<<<1, kUpdThreads, 0, st>>>(pre, st_in, beta, ctl, trace);
+  upd_weight_chunks<ZA><<<cb, kChunkThreads, 0, st>>>(za, w, n, beta, trace, pre);
+  upd_total_reduce<<<1, kUpdThreads, 0, st>>>(pre, trace);
+  upd_norm_chunks<<<cb, kChunkThreads, 0, st>>>(w, n, trace, pre);
+  upd_ess_reduce<<<1, kUpdThreads, 0, st>>>(pre, n, ess_frac, ctl, trace);
+  upd_cdf_chunks<<<cb, kChunkThreads, 0, st>>>(w, n, trace, pre);
+  upd_cdf_scan<<<1, kUpdThreads, 0, st>>>(pre, trace);
+  upd_cdf_fill<<<cb, kChunkThreads, 0, st>>>(w, n, trace, pre, scratch);
+  upd_resample<ZA><<<pb, 256, 0, st>>>(za, w, st_in, st_out, z_out, scratch, n, seed, k, trace);
+  upd_reset_weights<<<pb, 256, 0, st>>>(w, n, trace);
+  upd_est_chunks<<<cb, kChunkThreads, 0, st>>>(w, st_out, z_out, n, post);
+  upd_est_reduce<<<1, kUpdThreads, 0, st>>>(post, n, est_best, ctl, trace);
+}
+
+// ER_SMC_UPDATE_SINGLE=1 in the environment forces the single-CTA kernel at
+// every size (the bit-identity tests compare the two)
+bool update_multi(long long n) {
+  static const int single = [] {
+    const char* e = getenv("ER_SMC_UPDATE_SINGLE");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  return n >= kMultiMin && !single;
+}
+
 __global__ void argmax_update_kernel(const double* __restrict__ z, long long n,
                                      long long base, double* __restrict__ best) {
   __shared__ double shv[40];
@@ -567,9 +855,15 @@ extern "C" int er_smc_update(const double* z_dev, const uint8_t* degen_dev, doub
       !scratch_dev || !ctl_dev || !trace_row_dev || n < 1)
     return er_set_error(ER_EINVAL, "er_smc_update: args");
   if (beta < 0) return er_set_error(ER_EINVAL, "er_smc_update: beta must be >= 0");
-  smc_update_kernel<ZContig><<<1, kUpdThreads, 0, as_stream(stream)>>>(
-      ZContig{z_dev, degen_dev}, weights_dev, states_in_dev, states_out_dev, z_out_dev,
-      scratch_dev, n, beta, ess_fraction, seed, k, estimate_best, ctl_dev, trace_row_dev);
+  if (update_multi(n)) {
+    smc_update_multi(ZContig{z_dev, degen_dev}, weights_dev, states_in_dev, states_out_dev,
+                     z_out_dev, scratch_dev, n, beta, ess_fraction, seed, k, estimate_best,
+                     ctl_dev, trace_row_dev, as_stream(stream));
+  } else {
+    smc_update_kernel<ZContig><<<1, kUpdThreads, 0, as_stream(stream)>>>(
+        ZContig{z_dev, degen_dev}, weights_dev, states_in_dev, states_out_dev, z_out_dev,
+        scratch_dev, n, beta, ess_fraction, seed, k, estimate_best, ctl_dev, trace_row_dev);
+  }
   ER_CHECK_LAUNCH();
   return ER_OK;
 }
@@ -586,10 +880,16 @@ extern "C" int er_smc_update_gathered(const void* zd_dev, int64_t shard, int64_t
       block_bytes < 9 * shard || block_bytes % 8 != 0)
     return er_set_error(ER_EINVAL, "er_smc_update_gathered: args");
   if (beta < 0) return er_set_error(ER_EINVAL, "er_smc_update_gathered: beta must be >= 0");
-  smc_update_kernel<ZPacked><<<1, kUpdThreads, 0, as_stream(stream)>>>(
-      ZPacked{(const unsigned char*)zd_dev, shard, block_bytes}, weights_dev, states_in_dev,
-      states_out_dev, z_out_dev, scratch_dev, n, beta, ess_fraction, seed, k, estimate_best,
-      ctl_dev, trace_row_dev);
+  const ZPacked za{(const unsigned char*)zd_dev, shard, block_bytes};
+  if (update_multi(n)) {
+    smc_update_multi(za, weights_dev, states_in_dev, states_out_dev, z_out_dev, scratch_dev, n,
+                     beta, ess_fraction, seed, k, estimate_best, ctl_dev, trace_row_dev,
+                     as_stream(stream));
+  } else {
+    smc_update_kernel<ZPacked><<<1, kUpdThreads, 0, as_stream(stream)>>>(
+        za, weights_dev, states_in_dev, states_out_dev, z_out_dev, scratch_dev, n, beta,
+        ess_fraction, seed, k, estimate_best, ctl_dev, trace_row_dev);
+  }
   ER_CHECK_LAUNCH();
   return ER_OK;
 }

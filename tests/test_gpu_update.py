@@ -103,3 +103,92 @@ def test_best_tracking_strict_greater():
     assert ctl.has_best == 0          # 0.7 is not > 0.7
     _, _, _, _, ctl = _run_update(z, np.full(4, 0.25), st, 1.0, 1e-9, 0, 0, best=0.5)
     assert np.array_equal(np.array(ctl.best_state[:]), st[1])   # first max wins
+
+
+def _multi_case(n, beta, seed=5):
+    rng = np.random.default_rng(n + int(beta))
+    z = rng.random(n) ** 3
+    w = rng.random(n)
+    w /= w.sum()
+    states = rng.normal(size=(n, 6))
+    degen = (rng.random(n) < 0.01).astype(np.uint8)
+    return z, w, states, degen
+
+
+def _run_update_both(z, w, states, degen, beta, world=2):
+    """er_smc_update on contiguous arrays and er_smc_update_gathered on a
+    packed world-rank buffer ([z shard | flags shard | pad] per rank)."""
+    from paper_2504_19930_b200 import _lib
+    from paper_2504_19930_b200.device import ptr, require_cuda, stream_ptr
+    from paper_2504_19930_b200.smc import _u64
+
+    dev = require_cuda()
+    n = z.size
+    f64 = dict(dtype=torch.float64, device=dev)
+    out = []
+    for gathered in (False, True):
+        zt = torch.as_tensor(z, **f64)
+        dg = torch.as_tensor(degen, device=dev)
+        wt = torch.as_tensor(w, **f64)
+        st = torch.as_tensor(states, **f64)
+        so, zo, scratch = torch.empty_like(st), torch.empty_like(zt), torch.empty_like(zt)
+        trace = torch.zeros(_lib.ER_TRACE_STRIDE, **f64)
+        ctl = _lib.ErSmcCtl()
+        ctl.best_measurement = -1.0
+        ctl_t = torch.frombuffer(bytearray(bytes(memoryview(ctl))), dtype=torch.uint8).to(dev)
+        tail = (ptr(wt), ptr(st), ptr(so), ptr(zo), ptr(scratch), n, float(beta), 0.5,
+                _u64(3), 7, 0, ptr(ctl_t), ptr(trace), stream_ptr(dev))
+        if gathered:
+            shard = -(-n // world)
+            block = ((9 * shard + 7) // 8) * 8
+            buf = torch.zeros(world * block, dtype=torch.uint8, device=dev)
+            zp = np.zeros(world * shard)
+            zp[:n] = z
+            dp = np.zeros(world * shard, dtype=np.uint8)
+            dp[:n] = degen
+            for r in range(world):
+                seg = np.concatenate([zp[r * shard:(r + 1) * shard].view(np.uint8),
+                                      dp[r * shard:(r + 1) * shard]])
+                buf[r * block:r * block + seg.size] = torch.as_tensor(seg, device=dev)
+            _lib.call("er_smc_update_gathered", ptr(buf), shard, block, *tail)
+        else:
+            _lib.call("er_smc_update", ptr(zt), ptr(dg), *tail)
+        torch.cuda.synchronize()
+        out.append(np.concatenate([wt.cpu().numpy(), so.cpu().numpy().ravel(),
+                                   zo.cpu().numpy(), trace.cpu().numpy(),
+                                   np.frombuffer(ctl_t.cpu().numpy().tobytes(), np.float64)]))
+    return out
+
+
+_SINGLE_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from tests.test_gpu_update import _multi_case, _run_update_both
+z, w, s, d = _multi_case({n}, {beta})
+a, b = _run_update_both(z, w, s, d, {beta})
+np.save({path!r}, np.stack([a, b]))
+"""
+
+
+@pytest.mark.parametrize("n", [16384, 65537, 262144])
+@pytest.mark.parametrize("beta", [0.0, 50.0])
+def test_multi_cta_update_bit_identical(n, beta, tmp_path):
+    """At n >= 16384 the update runs as a chain of whole-GPU kernels (13
+    launches, same per-chunk loops and reduction trees); it must reproduce the
+    single-CTA kernel (forced with ER_SMC_UPDATE_SINGLE=1 in a subprocess)
+    bit for bit, contiguous and gathered, with and without resampling."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    z, w, s, d = _multi_case(n, beta)
+    multi = np.stack(_run_update_both(z, w, s, d, beta))
+    path = str(tmp_path / "single.npy")
+    env = dict(os.environ, ER_SMC_UPDATE_SINGLE="1")
+    subprocess.run([sys.executable, "-c", _SINGLE_SCRIPT.format(root=root, n=n, beta=beta,
+                                                                path=path)],
+                   check=True, env=env, cwd=root)
+    single = np.load(path)
+    assert np.array_equal(multi.view(np.uint64), single.view(np.uint64))
+    assert np.array_equal(multi[0], multi[1])          # gathered == contiguous
