@@ -1,5 +1,5 @@
 """register_smc at large particle counts (C5-style P) on the C2 pair: the
-single-CTA update with the CDF in global memory, workspace sizing, trace."""
+update (whole-GPU kernel chain at these sizes), workspace sizing, trace."""
 import os
 import sys
 import time
