@@ -17,7 +17,9 @@
 //   * fast paths (measure_oct_kernel): the source re-laid out per cell (8-bit
 //     "oct": 8 corners in one 8-byte word; binary "bit-oct": 8 corner bits;
 //     f32/f64 "quad": two float4 per sample), fixed-point coordinates from the
-//     reference's fp64 row start, fp32 lerps packed fp32x2 across voxel pairs
+//     reference's fp64 row start (in the pair / mask / fp64 loops stepped as
+//     fraction words + one padded cell index per voxel, PTX carry chains:
+//     cell_step), fp32 lerps packed fp32x2 across voxel pairs
 //     (or fp64 lerps in Q12.52 / Q24.40), fp32 row partials folded into fp64
 //     per row.  Generic path (measure_partials_kernel): 8 gathers per voxel,
 //     fp64 coordinates exactly as the reference, any storage / lerp mode.
