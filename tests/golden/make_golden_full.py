@@ -5,7 +5,7 @@ same grid).  Run in the build container only (/root/reference does not exist
 on the GPU box); about an hour of CPU at 8 numba threads:
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
-        python tests/golden/make_golden_full.py [c2] [c3]
+        python tests/golden/make_golden_full.py [c2] [c3] [c2o] [c2s:<seed> ...]
 
 Inputs are built with the reference's own generator (echoreg.phantom
 make_phantom / make_pair, phantom.py:61-166) on the echo grid of BASELINE
@@ -150,6 +150,30 @@ def c2o():
           est.to_array()[3:], flush=True)
 
 
+def c2s(seed):
+    """C2 (image mode, 2000 x 50) at another SMC seed, same pair: the
+    trajectory, resampling flags, ESS and the first iteration's likelihoods
+    (full_c2_seed<seed>.npz)."""
+    seed = int(seed)
+    tq, sq, _, _ = echo_case(1)
+    t = normalize_zscore(tq.frames[0])
+    s = normalize_zscore(sq.frames[0])
+    cfg = smc.SmcConfig(mode="image", n_particles=2000, n_iterations=50, seed=seed)
+    rec = RecordingExecutor(workers=int(os.environ["NUMBA_NUM_THREADS"]))
+    t0 = time.perf_counter()
+    est, trace = smc.register_smc(t, s, cfg, rec)
+    wall = time.perf_counter() - t0
+    out = {f"c2_{k}": v for k, v in trace_arrays(est, trace).items()}
+    out["c2_z_first"], out["c2_degen_first"] = rec.log[0]
+    out["c2_target_sha256"] = np.array(digest([tq.frames[0]]))
+    out["c2_source_sha256"] = np.array(digest([sq.frames[0]]))
+    out["c2_seed"] = np.array(seed)
+    out["c2_cpu_s"] = np.array(wall)
+    np.savez_compressed(os.path.join(OUT, f"full_c2_seed{seed}.npz"), **out)
+    print(f"full_c2_seed{seed}.npz", wall, "s; estimate deg", np.degrees(est.to_array()[:3]),
+          est.to_array()[3:], flush=True)
+
+
 def c3():
     tq, sq, tm, sm = echo_case(30)
     cfg = smc.SmcConfig(mode="mask", n_particles=2000, n_iterations=50, seed=0)
@@ -181,4 +205,5 @@ def c3():
 
 if __name__ == "__main__":
     for w in sys.argv[1:] or ["c2", "c3", "c2o"]:
-        globals()[w]()
+        name, _, arg = w.partition(":")   # c2s:<seed>
+        globals()[name](*([arg] if arg else []))

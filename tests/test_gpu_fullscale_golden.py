@@ -176,3 +176,54 @@ def test_c2_overlap_region_registration_matches_reference(c2, precision):
         assert np.array_equal(dd, dr), key
         rel = np.abs(zz - zr) / np.maximum(np.abs(zr), 1e-300)
         assert rel.max() <= Z_RTOL[precision], (key, float(rel.max()))
+
+
+def _seed_goldens():
+    import glob
+
+    return sorted(glob.glob(os.path.join(GOLDEN, "full_c2_seed*.npz")))
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+@pytest.mark.parametrize("path", _seed_goldens() or [None],
+                         ids=lambda p: os.path.basename(p) if p else "none")
+def test_c2_full_other_seeds_match_reference(c2, path, precision):
+    """C2 at further SMC seeds (tests/golden/full_c2_seed<s>.npz, the real
+    reference's register_smc).  f64 tracks the reference's whole trajectory
+    (same resampling decisions, estimates to 1e-9 degree); f32 holds the
+    north star's bar on the final transform (0.1 degree / 0.1 voxel) and the
+    per-particle likelihoods of the first iteration (1e-4), but may leave the
+    reference's trajectory at a resampling boundary later (SMC chaos,
+    DESIGN.md section 5 item 5) -- those seeds are kept, not skipped."""
+    from paper_2504_19930_b200 import Executor, SmcConfig
+    from paper_2504_19930_b200 import smc as dsmc
+
+    if path is None:
+        pytest.skip("no full_c2_seed*.npz generated")
+    g = np.load(path)
+    _, t, s = c2
+    assert str(g["c2_target_sha256"]) == str(c2[0]["c2_target_sha256"])
+    assert str(g["c2_source_sha256"]) == str(c2[0]["c2_source_sha256"])
+    cfg = SmcConfig(mode="image", n_particles=2000, n_iterations=50, seed=int(g["c2_seed"]))
+    run = dsmc.DeviceSmcRun(t, s, cfg, Executor(precision=precision))
+    z0 = None
+    for k in range(cfg.n_iterations):
+        run.predict(k)
+        run.measure()
+        if k == 0:
+            z0 = (run.z_local[:2000].cpu().numpy().copy(),
+                  run.dg_local[:2000].cpu().numpy().astype(bool))
+        run.update(k)
+    tr = run.finish()
+    rot, vox = _transform_diff(tr.estimates[-1].to_array(), g["c2_estimate"], t.spacing)
+    assert rot <= 0.1 and vox <= 0.1, (rot, vox)
+    assert np.array_equal(z0[1], g["c2_degen_first"])
+    rel = np.abs(z0[0] - g["c2_z_first"]) / np.maximum(np.abs(g["c2_z_first"]), 1e-300)
+    assert rel.max() <= Z_RTOL[precision], float(rel.max())
+    if precision == "f64":
+        assert np.array_equal(np.array(tr.resampled), g["c2_resampled"])
+        ess = np.array(tr.ess)
+        assert np.max(np.abs(ess - g["c2_ess"]) / g["c2_ess"]) <= ESS_RTOL["f64"]
+        est_all = np.stack([e.to_array() for e in tr.estimates])
+        traj = float(np.degrees(np.abs(est_all[:, :3] - g["c2_estimates"][:, :3])).max())
+        assert traj <= 1e-9, traj
