@@ -5,7 +5,7 @@ same grid).  Run in the build container only (/root/reference does not exist
 on the GPU box); about an hour of CPU at 8 numba threads:
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
-        python tests/golden/make_golden_full.py [c2] [c3] [c2o] [c2s:<seed> ...]
+        python tests/golden/make_golden_full.py [c2] [c3] [c2o] [c2s:<seed> ...] [c3s:<seed> ...]
 
 Inputs are built with the reference's own generator (echoreg.phantom
 make_phantom / make_pair, phantom.py:61-166) on the echo grid of BASELINE
@@ -174,9 +174,14 @@ def c2s(seed):
           est.to_array()[3:], flush=True)
 
 
-def c3():
+def c3s(seed):
+    """C3 at another SMC seed (full_c3_seed<seed>.npz, no report file)."""
+    c3(int(seed))
+
+
+def c3(seed=0):
     tq, sq, tm, sm = echo_case(30)
-    cfg = smc.SmcConfig(mode="mask", n_particles=2000, n_iterations=50, seed=0)
+    cfg = smc.SmcConfig(mode="mask", n_particles=2000, n_iterations=50, seed=seed)
     ex = Executor(workers=int(os.environ["NUMBA_NUM_THREADS"]))
     t0 = time.perf_counter()
     rep = register_sequence(tq, sq, tm, sm, cfg, ex, case_id="c3")
@@ -198,9 +203,14 @@ def c3():
         "c3_source_masks_sha256": np.array(digest(sm)),
         "c3_cpu_s": np.array(wall),
     }
-    np.savez_compressed(os.path.join(OUT, "full_c3.npz"), **out)
-    rep.save(os.path.join(OUT, "full_c3_report.json"))
-    print("full_c3.npz", wall, "s; estimate", rep.estimate_deg_mm, flush=True)
+    if seed:
+        out["c3_seed"] = np.array(seed)
+        np.savez_compressed(os.path.join(OUT, f"full_c3_seed{seed}.npz"), **out)
+    else:
+        np.savez_compressed(os.path.join(OUT, "full_c3.npz"), **out)
+        rep.save(os.path.join(OUT, "full_c3_report.json"))
+    print(f"full_c3_seed{seed}.npz" if seed else "full_c3.npz", wall, "s; estimate",
+          rep.estimate_deg_mm, flush=True)
 
 
 if __name__ == "__main__":
