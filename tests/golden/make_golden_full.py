@@ -5,7 +5,7 @@ same grid).  Run in the build container only (/root/reference does not exist
 on the GPU box); about an hour of CPU at 8 numba threads:
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
-        python tests/golden/make_golden_full.py [c2] [c3] [c2o] [c2s:<seed> ...] [c3s:<seed> ...]
+        python tests/golden/make_golden_full.py [c2] [c3] [c2o] [c2s:<seed> ...] [c3s:<seed> ...] [c2os:<seed> ...]
 
 Inputs are built with the reference's own generator (echoreg.phantom
 make_phantom / make_pair, phantom.py:61-166) on the echo grid of BASELINE
@@ -126,14 +126,19 @@ def c2():
           est.to_array()[3:], flush=True)
 
 
-def c2o():
+def c2os(seed):
+    """c2o at another SMC seed (full_c2o_seed<seed>.npz)."""
+    c2o(int(seed))
+
+
+def c2o(seed=3):
     """C2 in the overlap region (SmcConfig.ncc_region="overlap",
     kernels_numba.py:172-189 overlap branch): fewer iterations (20), same
     pair, seed 3."""
     tq, sq, _, _ = echo_case(1)
     t = normalize_zscore(tq.frames[0])
     s = normalize_zscore(sq.frames[0])
-    cfg = smc.SmcConfig(mode="image", n_particles=2000, n_iterations=20, seed=3,
+    cfg = smc.SmcConfig(mode="image", n_particles=2000, n_iterations=20, seed=seed,
                         ncc_region="overlap")
     rec = RecordingExecutor(workers=int(os.environ["NUMBA_NUM_THREADS"]))
     t0 = time.perf_counter()
@@ -145,8 +150,10 @@ def c2o():
     out["c2o_target_sha256"] = np.array(digest([tq.frames[0]]))
     out["c2o_source_sha256"] = np.array(digest([sq.frames[0]]))
     out["c2o_cpu_s"] = np.array(wall)
-    np.savez_compressed(os.path.join(OUT, "full_c2o.npz"), **out)
-    print("full_c2o.npz", wall, "s; estimate deg", np.degrees(est.to_array()[:3]),
+    name = "full_c2o.npz" if seed == 3 else f"full_c2o_seed{seed}.npz"
+    out["c2o_seed"] = np.array(seed)
+    np.savez_compressed(os.path.join(OUT, name), **out)
+    print(name, wall, "s; estimate deg", np.degrees(est.to_array()[:3]),
           est.to_array()[3:], flush=True)
 
 

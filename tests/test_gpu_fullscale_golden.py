@@ -138,22 +138,31 @@ def test_c3_full_4d_pipeline_matches_reference():
         assert got["aggregates"][k] == pytest.approx(v, rel=1e-6, abs=1e-9), k
 
 
+def _c2o_goldens():
+    import glob
+
+    return sorted(glob.glob(os.path.join(GOLDEN, "full_c2o*.npz")))
+
+
+@pytest.mark.parametrize("path", _c2o_goldens() or [None],
+                         ids=lambda p: os.path.basename(p) if p else "none")
 @pytest.mark.parametrize("precision", ["f32", "f64"])
-def test_c2_overlap_region_registration_matches_reference(c2, precision):
-    """The C2 pair with SmcConfig(ncc_region="overlap"), 2000 x 20, seed 3:
+def test_c2_overlap_region_registration_matches_reference(c2, precision, path):
+    """The C2 pair with SmcConfig(ncc_region="overlap"), 2000 x 20, seed 3
+    (and further seeds, full_c2o_seed<s>.npz):
     the overlap-region kernels (in-bounds target sums and sums of squares,
     /root/reference/pkg/src/echoreg/kernels_numba.py:172-189) against the real
     reference's run (tests/golden/full_c2o.npz)."""
     from paper_2504_19930_b200 import Executor, SmcConfig
     from paper_2504_19930_b200 import smc as dsmc
 
-    path = os.path.join(GOLDEN, "full_c2o.npz")
-    if not os.path.exists(path):
-        pytest.skip("full_c2o.npz not generated")
+    if path is None:
+        pytest.skip("full_c2o*.npz not generated")
     g = np.load(path)
     _, t, s = c2
     assert str(g["c2o_target_sha256"]) == str(c2[0]["c2_target_sha256"])
-    cfg = SmcConfig(mode="image", n_particles=2000, n_iterations=20, seed=3,
+    seed = int(g["c2o_seed"]) if "c2o_seed" in g else 3
+    cfg = SmcConfig(mode="image", n_particles=2000, n_iterations=20, seed=seed,
                     ncc_region="overlap")
     run = dsmc.DeviceSmcRun(t, s, cfg, Executor(precision=precision))
     z = {}
@@ -167,10 +176,17 @@ def test_c2_overlap_region_registration_matches_reference(c2, precision):
     tr = run.finish()
     rot, vox = _transform_diff(tr.estimates[-1].to_array(), g["c2o_estimate"], t.spacing)
     assert rot <= 0.1 and vox <= 0.1, (rot, vox)
-    assert np.array_equal(np.array(tr.resampled), g["c2o_resampled"])
-    ess = np.array(tr.ess)
-    assert np.max(np.abs(ess - g["c2o_ess"]) / g["c2o_ess"]) <= ESS_RTOL[precision]
+    # the seed-3 run is known to stay on the reference trajectory in every
+    # precision; at other seeds f32 may leave it at a resampling boundary
+    # (DESIGN.md section 5 item 5), so there only its first iteration is held
+    strict = precision != "f32" or seed == 3
+    if strict:
+        assert np.array_equal(np.array(tr.resampled), g["c2o_resampled"])
+        ess = np.array(tr.ess)
+        assert np.max(np.abs(ess - g["c2o_ess"]) / g["c2o_ess"]) <= ESS_RTOL[precision]
     for k, key in ((0, "first"), (cfg.n_iterations - 1, "last")):
+        if k and not strict:
+            continue
         zz, dd = z[k]
         zr, dr = g[f"c2o_z_{key}"], g[f"c2o_degen_{key}"]
         assert np.array_equal(dd, dr), key
